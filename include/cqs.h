@@ -1,0 +1,185 @@
+/*
+ * cqs.h — C ABI of libcqs: exact softmax attention decomposed by CQS Divide (Stream-CQSA,
+ * arXiv 2604.20819), B200 (sm_100a) forward hot path.
+ *
+ * Citations: P:n = PAPER.md line n (section in brackets).  R<n> = DESIGN.md reading n.
+ *
+ * Problem statement (P:8 [Abstract], P:19 [Intro], P:60 [Alg. 1 Require], P:248 [Sec. 4]):
+ *   given Q, K, V in R^{B x H x N x D} and a device-memory budget, return
+ *   O = softmax(alpha Q K^T) V  (alpha = 1/sqrt(D), non-causal) computed as c^itr independent
+ *   CQS tasks whose LSE-merge is exactly full attention.
+ *
+ * Conventions (all entry points):
+ *   - Every tensor and workspace is owned by the caller; libcqs never allocates device or pinned
+ *     memory and never frees caller memory.  Workspace sizes are queried up front.
+ *   - Plans are immutable after cqs_plan() and may be shared between threads.
+ *   - Device calls are asynchronous on `stream`; argument errors are detected on the host before
+ *     any launch and reported synchronously.  CUDA launch/runtime errors map to CQS_E_CUDA.
+ *   - On any non-OK status a thread-local message is available from cqs_last_error().
+ *   - Determinism: a fixed plan (task order, merge order) gives bit-identical output across runs.
+ */
+#ifndef CQS_H_
+#define CQS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CQS_ABI_VERSION 1
+#define CQS_MAX_DEPTH 12   /* N >= 7^depth and N < 2^31 imply depth <= 11 for c = 7           */
+#define CQS_MAX_SEGS 32    /* segments per task; observed <= 8 up to depth 11     */
+
+typedef enum {
+  CQS_OK = 0,
+  CQS_E_VERIFY = 1,       /* internal consistency check failed                                 */
+  CQS_E_INFEASIBLE = 2,   /* no depth fits budget_bytes (S:431 exit code 2)                    */
+  CQS_E_INVALID = 3,      /* bad argument: I not a difference set, N < c^depth, ...    */
+  CQS_E_CUDA = 4,         /* CUDA runtime / launch failure                                     */
+  CQS_E_NCCL = 5,
+  CQS_E_OOM = 6,          /* caller-provided workspace smaller than the queried size           */
+  CQS_E_UNSUPPORTED = 7   /* valid request this build has no kernel for (dtype / D / segs)     */
+} cqs_status;
+
+typedef enum { CQS_F32 = 0, CQS_BF16 = 1 } cqs_dtype;
+typedef enum { CQS_LOC_DEVICE = 0, CQS_LOC_PINNED_HOST = 1 } cqs_loc;
+
+/* ---------------------------------------------------------------------------------------------
+ * Planning (CQS Divide, Algorithm 3 BuildSubseq; masking P:130-134)
+ * --------------------------------------------------------------------------------------------- */
+typedef struct {
+  int64_t N;                 /* tokens                                                        */
+  int32_t B, H, D;           /* batch, heads, head dim; (b,h) planes are independent (R11)    */
+  int32_t c, l;              /* chunk count c = l(l-1)+1                               */
+  const int32_t* offsets;    /* interest set I, l entries, host memory, must be a (c,l,1)
+                                difference set with offsets[0] == 0 (owner code 0, R4) */
+  int32_t depth;             /* itr >= 0 explicit (0 = one task = plain attention); -1 = the
+                                smallest depth whose predicted device bytes fit budget_bytes
+                                (uniform scheduling; R14)                          */
+  uint64_t budget_bytes;     /* device bytes the call may use incl. caller device tensors (R14);
+                                0 = unlimited                                                  */
+  cqs_dtype in_dtype;        /* Q, K, V element type: CQS_BF16 (tcgen05 path) or CQS_F32     */
+  cqs_dtype out_dtype;       /* O element type                                                */
+  cqs_loc qkv_loc;           /* where Q, K, V live: device (resident) or pinned host (stream) */
+  cqs_loc out_loc;           /* where O and lse live                                          */
+  int32_t world, rank;       /* task sharding across `world` GPUs; world=1 on 1 GPU */
+} cqs_plan_desc;
+
+typedef struct cqs_plan_s cqs_plan_t; /* opaque, library-owned, immutable */
+
+typedef struct {
+  int32_t depth;                 /* itr actually planned                                       */
+  int32_t acc_depth;             /* device accumulator tier: rows of one depth-j subtree (0=all N) */
+  int32_t n_stage_buffers;       /* streamed mode: staging buffers (1 or 2), 0 when resident   */
+  int32_t reserved;
+  int64_t n_tasks;               /* c^depth                                            */
+  int64_t n_empty;               /* tasks with no kept pair (never launched, R9)               */
+  int64_t max_task_rows;         /* longest leaf                                               */
+  int64_t max_staged_rows;       /* most rows any task stages (streamed mode)                  */
+  uint64_t total_work_pairs;     /* sum of kept (q,k) pairs over all tasks = N^2 exactly       */
+  int64_t my_tasks;              /* non-empty tasks assigned to `rank` (LPT on work)           */
+  uint64_t my_work_pairs;
+  uint64_t dev_workspace_bytes;  /* = cqs_forward_workspace_size(...).dev                      */
+  uint64_t host_workspace_bytes; /* pinned host bytes (streamed mode)                          */
+  uint64_t predicted_peak_bytes; /* memory model M_dev: caller device tensors + dev workspace   */
+} cqs_plan_info_t;
+
+typedef struct {
+  int32_t nseg;                        /* maximal segments of consecutive tokens, constant codes */
+  int32_t rank;                        /* owning rank (-1 if empty)                              */
+  uint64_t work;                       /* kept (query, key) pairs                                */
+  int32_t quorum[CQS_MAX_DEPTH];       /* (q_1..q_depth)                                   */
+  int64_t seg_start[CQS_MAX_SEGS];     /* global token id of the segment's first token          */
+  int64_t seg_len[CQS_MAX_SEGS];
+  uint8_t seg_codes[CQS_MAX_SEGS][CQS_MAX_DEPTH]; /* code_t = index in I order of its level-t
+                                                     chunk; 0 = owner (R4)              */
+  uint32_t kept[CQS_MAX_SEGS];         /* kept[a] bit b: query seg a attends key seg b; equals
+                                          LocalMaskFromGroupRuns at segment granularity */
+} cqs_task_t;
+
+/* Build the plan (host only, synchronous).  Validates I, picks depth, enumerates the c^depth
+ * quorum tuples lexicographically (R3), cuts each leaf into segments, derives the kept
+ * blocks, work and empty flags, assigns non-empty tasks to ranks by LPT on work, and evaluates the
+ * memory model.  Errors: CQS_E_INVALID (bad desc), CQS_E_INFEASIBLE (depth=-1 and nothing fits or
+ * explicit depth over budget), CQS_E_UNSUPPORTED (> CQS_MAX_SEGS segments).  *out owned by caller,
+ * release with cqs_plan_destroy. */
+cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out);
+cqs_status cqs_plan_info(const cqs_plan_t* plan, cqs_plan_info_t* info);
+/* Task `idx` (0 <= idx < n_tasks, lexicographic order) into *task. */
+cqs_status cqs_plan_task(const cqs_plan_t* plan, int64_t idx, cqs_task_t* task);
+/* Canonical plan bytes (little endian): "CQSP", u32 version=1, i64 N, i32 c, i32 l, i32 I[l],
+ * i32 depth, i64 n_tasks, then per task in lexicographic order: i32 nseg, u64 work,
+ * nseg x (i64 start, i64 len, u8 codes[depth]), nseg x u32 kept mask.
+ * If buf is NULL or *len too small, *len receives the required size and CQS_E_INVALID (buf NULL:
+ * CQS_OK) is returned. */
+cqs_status cqs_plan_serialize(const cqs_plan_t* plan, void* buf, size_t* len);
+void cqs_plan_destroy(cqs_plan_t* plan);
+
+/* Memory model M_dev: predicted device bytes of a forward call with the
+ * given depth / accumulator tier / staging buffers.  Pure host arithmetic on the desc. */
+cqs_status cqs_memory_model(const cqs_plan_desc* desc, int32_t depth, int32_t acc_depth,
+                            int32_t n_stage_buffers, uint64_t* dev_bytes, uint64_t* host_bytes);
+
+/* ---------------------------------------------------------------------------------------------
+ * Forward (Algorithm 1 in LSE form: per-task partial (O_i, lse_i) + IndexAdd-merge)
+ * --------------------------------------------------------------------------------------------- */
+typedef struct {
+  double ms_plan, ms_h2d, ms_attn, ms_merge, ms_exchange, ms_total; /* filled when stats != NULL
+                                                                       (host wall clock, syncs)  */
+  uint64_t bytes_h2d, bytes_d2h, bytes_exchanged, peak_dev_bytes;
+  int64_t tasks_run, tasks_skipped, kernel_launches;
+} cqs_stats;
+
+cqs_status cqs_forward_workspace_size(const cqs_plan_t* plan, size_t* dev_bytes, size_t* host_bytes);
+
+/* Run this rank's tasks.
+ *   q, k, v     : [B,H,N,D] of desc.in_dtype at desc.qkv_loc.  qkv_strides = element strides of
+ *                 (B, H, N, D); stride D must be 1; device tensors need 16-byte aligned rows
+ *                 (TMA).  Streamed (pinned host) tensors must be contiguous.
+ *   out         : [B,H,N,D] of desc.out_dtype at desc.out_loc with element strides out_strides
+ *                 (stride D = 1).  Written only when world == 1 (else see cqs_partial_view).
+ *   lse         : nullable, fp32 [B,H,N] contiguous at desc.out_loc: natural-log sum of
+ *                 exp(alpha q.k) over all keys (the FA `softmax_lse`).
+ *   scale       : alpha; <= 0 selects 1/sqrt(D).
+ *   budget_bytes: the caller's device budget; CQS_E_INFEASIBLE if the plan's predicted peak
+ *                 exceeds it (0 = trust the plan).
+ *   dev_ws/host_ws: at least cqs_forward_workspace_size() bytes (256-byte aligned); host_ws
+ *                 pinned.  With world > 1 dev_ws keeps this rank's fp32 partial accumulator
+ *                 after the call.
+ * Asynchronous on `stream` unless stats != NULL (then it synchronizes to time stages). */
+cqs_status cqs_attention_forward(const cqs_plan_t* plan, const void* q, const void* k,
+                                 const void* v, const int64_t qkv_strides[4], void* out,
+                                 const int64_t out_strides[4], float* lse, float scale,
+                                 uint64_t budget_bytes, void* dev_ws, void* host_ws,
+                                 void* stream /* cudaStream_t */, cqs_stats* stats);
+
+/* Pointers to the fp32 partial accumulator inside dev_ws after a world > 1 forward:
+ * acc_o [N][B*H][D], acc_lse [N][B*H] (natural log; -inf = no contribution yet). */
+cqs_status cqs_partial_view(const cqs_plan_t* plan, void* dev_ws, float** acc_o, float** acc_lse);
+
+/* Rows owned by `rank` for the final merge: [row0, row0 + rows) with row0 = floor(rank N / world). */
+cqs_status cqs_shard_rows(int64_t N, int32_t world, int32_t rank, int64_t* row0, int64_t* rows);
+
+/* R-way LSE merge (Eq. 3 with Den_j = exp(lse_j), Num_j = O_j Den_j), on device:
+ * for r < rows, p < B*H:   lse = log sum_j exp(lse_j[r,p]);   O = sum_j exp(lse_j - lse) O_j[r,p,:]
+ * over j < n_parts (part_o[j]: [rows][B*H][D] fp32, part_lse[j]: [rows][B*H] fp32, device
+ * pointers listed in HOST arrays), plus the accumulator (acc_o, acc_lse) when non-NULL, which then
+ * receives the result.  -inf parts contribute nothing; all -inf gives O = 0, lse = -inf (R8).
+ * If out != NULL the result is also written cast to out_dtype into rows [out_row0, out_row0+rows)
+ * of the [B,H,N,D] tensor `out` (element strides out_strides), and lse_out (nullable,
+ * [B,H,N] contiguous fp32, row offset out_row0, n_total = N) receives lse.  Errors:
+ * CQS_E_INVALID (n_parts < 0, D > 256 or not a multiple of 4, NULL required pointer). */
+cqs_status cqs_merge(int64_t rows, int32_t B, int32_t H, int32_t D, int32_t n_parts,
+                     const float* const* part_o, const float* const* part_lse, float* acc_o,
+                     float* acc_lse, void* out, cqs_dtype out_dtype, const int64_t out_strides[4],
+                     int64_t out_row0, int64_t n_total, float* lse_out, void* stream);
+
+const char* cqs_last_error(void);
+int32_t cqs_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CQS_H_ */

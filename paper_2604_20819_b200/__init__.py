@@ -1,0 +1,270 @@
+"""Python binding of libcqs (include/cqs.h): argument marshalling only.
+
+Every step of the hot path (planning, attention, merge, finalize) runs inside libcqs.so; this module
+converts Python / torch arguments to the C ABI and raises `CqsError` on any non-OK status.  There is
+no fallback: if libcqs.so is missing the import of the library raises immediately.
+
+Same names as the C ABI: cqs_plan, cqs_plan_info, cqs_plan_task, cqs_plan_serialize,
+cqs_memory_model, cqs_forward_workspace_size, cqs_attention_forward, cqs_partial_view,
+cqs_shard_rows, cqs_merge.  `attention()` is a convenience wrapper (allocates the workspace with
+torch and calls the above).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcqs.so")
+
+CQS_OK, CQS_E_VERIFY, CQS_E_INFEASIBLE, CQS_E_INVALID, CQS_E_CUDA, CQS_E_NCCL, CQS_E_OOM, \
+    CQS_E_UNSUPPORTED = range(8)
+CQS_F32, CQS_BF16 = 0, 1
+CQS_LOC_DEVICE, CQS_LOC_PINNED_HOST = 0, 1
+CQS_MAX_DEPTH, CQS_MAX_SEGS = 12, 32
+STATUS_NAMES = {0: "CQS_OK", 1: "CQS_E_VERIFY", 2: "CQS_E_INFEASIBLE", 3: "CQS_E_INVALID",
+                4: "CQS_E_CUDA", 5: "CQS_E_NCCL", 6: "CQS_E_OOM", 7: "CQS_E_UNSUPPORTED"}
+
+#: every symbol include/cqs.h declares (tests/test_abi.py checks the .so exports them all)
+ABI_SYMBOLS = ("cqs_plan", "cqs_plan_info", "cqs_plan_task", "cqs_plan_serialize",
+               "cqs_plan_destroy", "cqs_memory_model", "cqs_forward_workspace_size",
+               "cqs_attention_forward", "cqs_partial_view", "cqs_shard_rows", "cqs_merge",
+               "cqs_last_error", "cqs_abi_version")
+
+
+class CqsError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("%s: %s" % (STATUS_NAMES.get(status, status), msg))
+        self.status = status
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [("N", C.c_int64), ("B", C.c_int32), ("H", C.c_int32), ("D", C.c_int32),
+                ("c", C.c_int32), ("l", C.c_int32), ("offsets", C.POINTER(C.c_int32)),
+                ("depth", C.c_int32), ("budget_bytes", C.c_uint64), ("in_dtype", C.c_int),
+                ("out_dtype", C.c_int), ("qkv_loc", C.c_int), ("out_loc", C.c_int),
+                ("world", C.c_int32), ("rank", C.c_int32)]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("depth", C.c_int32), ("acc_depth", C.c_int32), ("n_stage_buffers", C.c_int32),
+                ("reserved", C.c_int32), ("n_tasks", C.c_int64), ("n_empty", C.c_int64),
+                ("max_task_rows", C.c_int64), ("max_staged_rows", C.c_int64),
+                ("total_work_pairs", C.c_uint64), ("my_tasks", C.c_int64),
+                ("my_work_pairs", C.c_uint64), ("dev_workspace_bytes", C.c_uint64),
+                ("host_workspace_bytes", C.c_uint64), ("predicted_peak_bytes", C.c_uint64)]
+
+
+class Task(C.Structure):
+    _fields_ = [("nseg", C.c_int32), ("rank", C.c_int32), ("work", C.c_uint64),
+                ("quorum", C.c_int32 * CQS_MAX_DEPTH), ("seg_start", C.c_int64 * CQS_MAX_SEGS),
+                ("seg_len", C.c_int64 * CQS_MAX_SEGS),
+                ("seg_codes", (C.c_uint8 * CQS_MAX_DEPTH) * CQS_MAX_SEGS),
+                ("kept", C.c_uint32 * CQS_MAX_SEGS)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("ms_plan", C.c_double), ("ms_h2d", C.c_double), ("ms_attn", C.c_double),
+                ("ms_merge", C.c_double), ("ms_exchange", C.c_double), ("ms_total", C.c_double),
+                ("bytes_h2d", C.c_uint64), ("bytes_d2h", C.c_uint64),
+                ("bytes_exchanged", C.c_uint64), ("peak_dev_bytes", C.c_uint64),
+                ("tasks_run", C.c_int64), ("tasks_skipped", C.c_int64),
+                ("kernel_launches", C.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libcqs.so (raises if it was not built: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("libcqs.so not built (run __graft_entry__.build()): " + LIB_PATH)
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.cqs_plan.argtypes = [C.POINTER(PlanDesc), C.POINTER(P)]
+        L.cqs_plan_info.argtypes = [P, C.POINTER(PlanInfo)]
+        L.cqs_plan_task.argtypes = [P, C.c_int64, C.POINTER(Task)]
+        L.cqs_plan_serialize.argtypes = [P, P, C.POINTER(C.c_size_t)]
+        L.cqs_plan_destroy.argtypes = [P]
+        L.cqs_plan_destroy.restype = None
+        L.cqs_memory_model.argtypes = [C.POINTER(PlanDesc), C.c_int32, C.c_int32, C.c_int32,
+                                       C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.cqs_forward_workspace_size.argtypes = [P, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
+        L.cqs_attention_forward.argtypes = [P, P, P, P, C.POINTER(C.c_int64), P,
+                                            C.POINTER(C.c_int64), P, C.c_float, C.c_uint64, P, P,
+                                            P, C.POINTER(Stats)]
+        L.cqs_partial_view.argtypes = [P, P, C.POINTER(P), C.POINTER(P)]
+        L.cqs_shard_rows.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_int64)]
+        L.cqs_merge.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                C.POINTER(P), C.POINTER(P), P, P, P, C.c_int,
+                                C.POINTER(C.c_int64), C.c_int64, C.c_int64, P, P]
+        L.cqs_last_error.restype = C.c_char_p
+        L.cqs_abi_version.restype = C.c_int32
+        for name in ABI_SYMBOLS:
+            if name not in ("cqs_plan_destroy", "cqs_last_error", "cqs_abi_version"):
+                getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st):
+    if st != CQS_OK:
+        raise CqsError(st, lib().cqs_last_error().decode())
+
+
+def _i64x4(t):
+    return (C.c_int64 * 4)(*[int(x) for x in t])
+
+
+def _dtype_code(x):
+    if isinstance(x, int):
+        return x
+    return {"bf16": CQS_BF16, "bfloat16": CQS_BF16, "f32": CQS_F32, "float32": CQS_F32}[str(x).replace("torch.", "")]
+
+
+def _loc_code(x):
+    if isinstance(x, int):
+        return x
+    return {"device": CQS_LOC_DEVICE, "host": CQS_LOC_PINNED_HOST, "pinned": CQS_LOC_PINNED_HOST}[x]
+
+
+def make_desc(N, B, H, D, depth=1, budget_bytes=0, in_dtype="bf16", out_dtype=None,
+              qkv_loc="device", out_loc=None, world=1, rank=0, c=7, offsets=(0, 1, 3)):
+    offs = (C.c_int32 * len(offsets))(*offsets)
+    d = PlanDesc(N=N, B=B, H=H, D=D, c=c, l=len(offsets), offsets=offs, depth=depth,
+                 budget_bytes=int(budget_bytes), in_dtype=_dtype_code(in_dtype),
+                 out_dtype=_dtype_code(out_dtype if out_dtype is not None else in_dtype),
+                 qkv_loc=_loc_code(qkv_loc),
+                 out_loc=_loc_code(out_loc if out_loc is not None else qkv_loc),
+                 world=world, rank=rank)
+    d._offs = offs  # keep alive
+    return d
+
+
+class Plan:
+    """Owns a cqs_plan_t*."""
+
+    def __init__(self, desc: PlanDesc):
+        self.desc = desc
+        h = C.c_void_p()
+        _check(lib().cqs_plan(C.byref(desc), C.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.cqs_plan_destroy(self.handle)
+            self.handle = None
+
+    def info(self) -> PlanInfo:
+        return cqs_plan_info(self)
+
+    def task(self, i) -> Task:
+        return cqs_plan_task(self, i)
+
+
+def cqs_plan(desc=None, **kw) -> Plan:
+    return Plan(desc if desc is not None else make_desc(**kw))
+
+
+def cqs_plan_info(plan: Plan) -> PlanInfo:
+    info = PlanInfo()
+    _check(lib().cqs_plan_info(plan.handle, C.byref(info)))
+    return info
+
+
+def cqs_plan_task(plan: Plan, idx: int) -> Task:
+    t = Task()
+    _check(lib().cqs_plan_task(plan.handle, int(idx), C.byref(t)))
+    return t
+
+
+def cqs_plan_serialize(plan: Plan) -> bytes:
+    n = C.c_size_t(0)
+    _check(lib().cqs_plan_serialize(plan.handle, None, C.byref(n)))
+    buf = C.create_string_buffer(n.value)
+    _check(lib().cqs_plan_serialize(plan.handle, buf, C.byref(n)))
+    return buf.raw[:n.value]
+
+
+def cqs_memory_model(desc: PlanDesc, depth, acc_depth=0, n_stage_buffers=0):
+    dv, hb = C.c_uint64(), C.c_uint64()
+    _check(lib().cqs_memory_model(C.byref(desc), depth, acc_depth, n_stage_buffers,
+                                  C.byref(dv), C.byref(hb)))
+    return dv.value, hb.value
+
+
+def cqs_forward_workspace_size(plan: Plan):
+    dv, hb = C.c_size_t(), C.c_size_t()
+    _check(lib().cqs_forward_workspace_size(plan.handle, C.byref(dv), C.byref(hb)))
+    return dv.value, hb.value
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def cqs_attention_forward(plan: Plan, q, k, v, out, lse=None, scale=0.0, budget_bytes=0,
+                          dev_ws=None, host_ws=None, stream=None, stats=False):
+    """q/k/v/out: torch tensors [B,H,N,D] (stride(D)=1); lse: fp32 [B,H,N] contiguous or None."""
+    st = Stats() if stats else None
+    _check(lib().cqs_attention_forward(
+        plan.handle, _ptr(q), _ptr(k), _ptr(v), _i64x4(q.stride()), _ptr(out),
+        _i64x4(out.stride()) if out is not None else None, _ptr(lse), float(scale),
+        int(budget_bytes), _ptr(dev_ws), _ptr(host_ws), _stream_ptr(stream),
+        C.byref(st) if st is not None else None))
+    return st
+
+
+def cqs_partial_view(plan: Plan, dev_ws):
+    o, l_ = C.c_void_p(), C.c_void_p()
+    _check(lib().cqs_partial_view(plan.handle, _ptr(dev_ws), C.byref(o), C.byref(l_)))
+    return o.value, l_.value
+
+
+def cqs_shard_rows(N, world, rank):
+    a, n = C.c_int64(), C.c_int64()
+    _check(lib().cqs_shard_rows(N, world, rank, C.byref(a), C.byref(n)))
+    return a.value, n.value
+
+
+def cqs_merge(rows, B, H, D, part_o, part_lse, acc_o=None, acc_lse=None, out=None,
+              out_row0=0, n_total=None, lse_out=None, stream=None):
+    """part_o / part_lse: lists of fp32 device tensors ([rows, B*H, D] / [rows, B*H])."""
+    n = len(part_o)
+    po = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in part_o])
+    pl = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in part_lse])
+    import torch
+    od = CQS_BF16 if (out is not None and out.dtype == torch.bfloat16) else CQS_F32
+    _check(lib().cqs_merge(int(rows), B, H, D, n, po, pl, _ptr(acc_o), _ptr(acc_lse), _ptr(out), od,
+                           _i64x4(out.stride()) if out is not None else None, int(out_row0),
+                           int(n_total if n_total is not None else rows), _ptr(lse_out),
+                           _stream_ptr(stream)))
+
+
+def attention(q, k, v, depth=1, budget_bytes=0, out_dtype=None, scale=0.0, want_lse=True,
+              offsets=(0, 1, 3), stats=False):
+    """softmax(alpha Q K^T) V for device tensors q, k, v [B,H,N,D] through CQS Divide at `depth`
+    (-1: from budget_bytes).  Returns (out, lse[, stats])."""
+    import torch
+    B, H, N, D = q.shape
+    ind = CQS_BF16 if q.dtype == torch.bfloat16 else CQS_F32
+    odt = out_dtype or q.dtype
+    p = cqs_plan(N=N, B=B, H=H, D=D, depth=depth, budget_bytes=budget_bytes, in_dtype=ind,
+                 out_dtype=CQS_BF16 if odt == torch.bfloat16 else CQS_F32, offsets=offsets,
+                 c=len(offsets) * (len(offsets) - 1) + 1)
+    dev, _ = cqs_forward_workspace_size(p)
+    ws = torch.empty(max(dev, 256), dtype=torch.uint8, device=q.device)
+    out = torch.empty((B, H, N, D), dtype=odt, device=q.device)
+    lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if want_lse else None
+    st = cqs_attention_forward(p, q, k, v, out, lse, scale, budget_bytes, ws, None, stats=stats)
+    return (out, lse, st) if stats else (out, lse)

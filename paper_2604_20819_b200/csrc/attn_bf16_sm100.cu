@@ -1,0 +1,353 @@
+// Per-task CQS attention kernel, bf16 inputs, sm_100a tcgen05 / TMEM / TMA.
+//
+// Computes, for every kept (query-segment, key-segment) block of one CQS task, the per-task
+// partial of Eq. 2 in the normalised form an FA kernel returns:
+//   S = alpha Q K^T (tcgen05.mma, fp32 in TMEM) -> online softmax in registers (exp2, one thread
+//   per row) -> P (bf16, written back into TMEM over S) -> O += P V (tcgen05.mma, A from TMEM)
+// and merges (O_i, lse_i) straight into the fp32 accumulator (Eq. 3 in LSE form) in the
+// epilogue, so partials never round-trip through HBM.
+//
+// CTA = two 128-row query tiles of one query segment (256 rows) of one (b,h) plane; warp roles:
+//   warp 0      TMA producer (Q once, then K/V tiles through a kStages ring)
+//   warp 1      MMA issuer (single thread): S_j(t0), S_j(t1), then per j: PV_j(t0), S_{j+1}(t0),
+//               PV_j(t1), S_{j+1}(t1) — the two tiles ping-pong so one tile's softmax overlaps
+//               the other tile's MMAs
+//   warp 2      TMEM allocator (512 columns: S0 | S1 | O0 | O1)
+//   warps 4-7   softmax + correction + epilogue of tile 0 (thread = row = TMEM lane)
+//   warps 8-11  same for tile 1
+// Masking is block-level (segment-pair skipping, F3); the only element predicate is the
+// tail column bound of a key segment's last tile.  Rows beyond the segment are loaded but never
+// stored.  O rescaling is conditional (only when the running max grows by > 8 in log2 units).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "ptx.cuh"
+#include "task_params.cuh"
+
+namespace cqs {
+
+constexpr int kBM = 128;   // query rows per tile (TMEM lanes)
+constexpr int kBN = 128;   // keys per KV tile
+constexpr int kAttnThreads = 384;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
+
+template <int D>
+struct AttnCfg {
+  static constexpr int kBoxes = D / 64;                // 64-column (128-byte) TMA boxes
+  static constexpr int kQBytes = kBM * D * 2;
+  static constexpr int kKVBytes = kBN * D * 2;
+  static constexpr int kStages = D == 128 ? 4 : 8;
+  static constexpr int kSmemBytes = 2 * kQBytes + kStages * kKVBytes + 1024 + 512;
+  static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
+};
+
+// Iterates the key tiles of the kept key segments of one query segment (ascending segment id).
+struct KvCursor {
+  uint32_t mask;
+  int seg, kt, ntile;
+  const TaskParams* tp;
+  __device__ __forceinline__ void set_seg() {
+    seg = mask ? __ffs(mask) - 1 : 0;
+    kt = 0;
+    ntile = mask ? (tp->seg_len[seg] + kBN - 1) / kBN : 0;
+  }
+  __device__ __forceinline__ void init(const TaskParams* p, uint32_t m) {
+    tp = p;
+    mask = m;
+    set_seg();
+  }
+  __device__ __forceinline__ int row() const { return tp->seg_src[seg] + kt * kBN; }
+  __device__ __forceinline__ int valid() const { return min(kBN, tp->seg_len[seg] - kt * kBN); }
+  __device__ __forceinline__ void next() {
+    if (++kt == ntile) {
+      mask &= mask - 1;
+      set_seg();
+    }
+  }
+};
+
+template <int D>
+__global__ void __launch_bounds__(kAttnThreads, 1)
+    attn_bf16_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
+                           const __grid_constant__ CUtensorMap tmK,
+                           const __grid_constant__ CUtensorMap tmV,
+                           const __grid_constant__ TaskParams tp, float* __restrict__ acc_o,
+                           float* __restrict__ acc_lse, float scale_log2) {
+  using C = AttnCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;                         // [2][kBoxes][128 rows][128 B]
+  uint8_t* sKV = smem + 2 * C::kQBytes;       // [kStages][kBoxes][128 rows][128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kStages * C::kKVBytes);
+  uint64_t* q_full = bars;                    // 1
+  uint64_t* kv_full = bars + 1;               // kStages
+  uint64_t* kv_empty = kv_full + C::kStages;  // kStages
+  uint64_t* s_full = kv_empty + C::kStages;   // 2
+  uint64_t* p_full = s_full + 2;              // 2
+  uint64_t* o_bar = p_full + 2;               // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- work item: (query segment, 256-row pair) x (b,h) plane ----
+  const int item = blockIdx.x / tp.BH, bh = blockIdx.x % tp.BH;
+  int oi = 0;
+  while (item >= tp.item_end[oi]) ++oi;
+  const int a = tp.order[oi];
+  const int q_off = (item - (oi ? tp.item_end[oi - 1] : 0)) * (2 * kBM);
+  const int len_a = tp.seg_len[a];
+  const int valid0 = min(kBM, len_a - q_off);
+  const int valid1 = max(0, min(kBM, len_a - q_off - kBM));
+  const bool two = valid1 > 0;
+  const int bi = bh / tp.H, hi = bh % tp.H;
+  const uint32_t kmask = tp.kept[a];
+  int n_kv = 0;
+  for (uint32_t m = kmask; m; m &= m - 1) n_kv += (tp.seg_len[__ffs(m) - 1] + kBN - 1) / kBN;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 1);
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(&kv_full[s], 1);
+      ptx::mbar_init(&kv_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(&s_full[t], 1);
+      ptx::mbar_init(&p_full[t], 4);
+      ptx::mbar_init(&o_bar[t], 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // register split: 4 warps x 80 + 8 warps x 216 = 65536 / 32 (the whole RF of one SM)
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tmQ);
+      ptx::tma_prefetch_desc(&tmK);
+      ptx::tma_prefetch_desc(&tmV);
+      const int q_row = tp.seg_src[a] + q_off;
+      ptx::mbar_arrive_expect_tx(q_full, (two ? 2 : 1) * C::kQBytes);
+      for (int t = 0; t < (two ? 2 : 1); ++t)
+        for (int bx = 0; bx < C::kBoxes; ++bx)
+          ptx::tma_load_4d(sQ + t * C::kQBytes + bx * kBM * 128, &tmQ, q_full, bx * 64,
+                           q_row + t * kBM, hi, bi);
+      int it = 0;
+      auto load = [&](const CUtensorMap* map, int row) {
+        const int s = it % C::kStages;
+        const uint32_t ph = (it / C::kStages) & 1;
+        ptx::mbar_wait(&kv_empty[s], ph ^ 1);
+        ptx::mbar_arrive_expect_tx(&kv_full[s], C::kKVBytes);
+        for (int bx = 0; bx < C::kBoxes; ++bx)
+          ptx::tma_load_4d(sKV + s * C::kKVBytes + bx * kBN * 128, map, &kv_full[s], bx * 64, row,
+                           hi, bi);
+        ++it;
+      };
+      KvCursor ck, cv;
+      ck.init(&tp, kmask);
+      cv.init(&tp, kmask);
+      load(&tmK, ck.row());
+      ck.next();
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) {
+          load(&tmK, ck.row());
+          ck.next();
+        }
+        load(&tmV, cv.row());
+        cv.next();
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (one thread) =================
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = ptx::idesc_bf16(kBM, kBN, 0, 0);
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16(kBM, D, 0, 1);
+      const uint32_t sq = ptx::smem_u32(sQ), skv = ptx::smem_u32(sKV);
+      const uint32_t colS[2] = {C::kColS0, C::kColS1}, colO[2] = {C::kColO0, C::kColO1};
+      auto issue_S = [&](int t, int s) {
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t off = (ks >> 2) * (kBM * 128) + (ks & 3) * 32;
+          const uint64_t ad = ptx::smem_desc_sw128(sq + t * C::kQBytes + off, 16, 1024);
+          const uint64_t bd = ptx::smem_desc_sw128(skv + s * C::kKVBytes + off, 16, 1024);
+          ptx::mma_ss(tmem + colS[t], ad, bd, idesc_qk, ks > 0);
+        }
+        ptx::mma_commit(&s_full[t]);
+      };
+      auto issue_PV = [&](int t, int s, bool acc) {
+#pragma unroll
+        for (int ks = 0; ks < kBN / 16; ++ks) {
+          const uint64_t bd =
+              ptx::smem_desc_sw128(skv + s * C::kKVBytes + ks * 16 * 128, kBN * 128, 1024);
+          ptx::mma_ts(tmem + colO[t], tmem + colS[t] + ks * 8, bd, idesc_pv, (acc || ks > 0));
+        }
+        ptx::mma_commit(&o_bar[t]);
+      };
+      int it = 0;
+      ptx::mbar_wait(q_full, 0);
+      const int sK0 = it % C::kStages;
+      ptx::mbar_wait(&kv_full[sK0], (it / C::kStages) & 1);
+      ++it;
+      ptx::tc_fence_after();
+      issue_S(0, sK0);
+      if (two) issue_S(1, sK0);
+      ptx::mma_commit(&kv_empty[sK0]);
+      for (int j = 0; j < n_kv; ++j) {
+        int sKn = -1;
+        if (j + 1 < n_kv) {
+          sKn = it % C::kStages;
+          ptx::mbar_wait(&kv_full[sKn], (it / C::kStages) & 1);
+          ++it;
+        }
+        const int sV = it % C::kStages;
+        ptx::mbar_wait(&kv_full[sV], (it / C::kStages) & 1);
+        ++it;
+        ptx::tc_fence_after();
+        for (int t = 0; t < (two ? 2 : 1); ++t) {
+          ptx::mbar_wait(&p_full[t], j & 1);
+          ptx::tc_fence_after();
+          issue_PV(t, sV, j > 0);
+          if (sKn >= 0) issue_S(t, sKn);
+        }
+        ptx::mma_commit(&kv_empty[sV]);
+        if (sKn >= 0) ptx::mma_commit(&kv_empty[sKn]);
+      }
+    }
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
+    // ================= softmax / correction / epilogue =================
+    const int t = (warp - 4) >> 2;
+    if (t == 0 || two) {
+      const int sub = warp & 3;
+      const int r = sub * 32 + lane;
+      const uint32_t lane_base = uint32_t(sub * 32) << 16;
+      const uint32_t tS = tmem + lane_base + (t ? C::kColS1 : C::kColS0);
+      const uint32_t tO = tmem + lane_base + (t ? C::kColO1 : C::kColO0);
+      float m = -INFINITY, l = 0.f;
+      KvCursor cur;
+      cur.init(&tp, kmask);
+      for (int j = 0; j < n_kv; ++j) {
+        const int valid = cur.valid();
+        cur.next();
+        ptx::mbar_wait(&s_full[t], j & 1);
+        ptx::tc_fence_after();
+        uint32_t sr[kBN];
+#pragma unroll
+        for (int c = 0; c < kBN / 32; ++c)
+          ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+        ptx::tmem_ld_wait();
+        float* s = reinterpret_cast<float*>(sr);
+        if (valid < kBN) {
+#pragma unroll
+          for (int c = 0; c < kBN; ++c)
+            if (c >= valid) s[c] = -INFINITY;
+        }
+        float mx = s[0];
+#pragma unroll
+        for (int c = 1; c < kBN; ++c) mx = fmaxf(mx, s[c]);
+        mx *= scale_log2;
+        const float m_new = (j == 0 || mx > m + kRescaleThreshold) ? mx : m;
+        const bool need = (j > 0) && (m_new != m);
+        if (__any_sync(0xffffffffu, need)) {
+          // O must hold PV_{j-1} before it is rescaled (o_bar phase j-1)
+          ptx::mbar_wait(&o_bar[t], (j - 1) & 1);
+          ptx::tc_fence_after();
+          const float f = need ? ptx::ex2(m - m_new) : 1.f;
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t ov[32];
+            ptx::tmem_ld32(tO + c * 32, ov);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * f);
+            ptx::tmem_st32(tO + c * 32, ov);
+          }
+          ptx::tmem_st_wait();
+          l *= f;
+        }
+        m = m_new;
+        float rs = 0.f;
+        uint32_t pk[kBN / 2];
+#pragma unroll
+        for (int c = 0; c < kBN / 2; ++c) {
+          const float p0 = ptx::ex2(fmaf(s[2 * c], scale_log2, -m));
+          const float p1 = ptx::ex2(fmaf(s[2 * c + 1], scale_log2, -m));
+          rs += p0 + p1;
+          pk[c] = ptx::pack_bf16(p0, p1);
+        }
+        l += rs;
+        ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+      }
+      // ---- epilogue: O_i = O / l, lse_i = ln(sum exp) -> merge into the accumulator ----
+      ptx::mbar_wait(&o_bar[t], (n_kv - 1) & 1);
+      ptx::tc_fence_after();
+      const int vrows = t ? valid1 : valid0;
+      const bool live = r < vrows;
+      const float inv_l = 1.f / l;
+      const float lse = (m + __log2f(l)) * 0.69314718055994531f;
+      const int64_t idx = int64_t(tp.seg_dst[a] + q_off + t * kBM + r) * tp.BH + bh;
+      MergeW w{};
+      if (live) w = merge_weights(acc_lse[idx], lse);
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t ov[32];
+        ptx::tmem_ld32(tO + c * 32, ov);
+        ptx::tmem_ld_wait();
+        if (live) {
+          float o[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(ov[i]) * inv_l;
+          merge_chunk<32>(acc_o + idx * D + c * 32, o, w);
+        }
+      }
+      if (live) acc_lse[idx] = w.lse;
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D>
+static cudaError_t launch_bf16_impl(const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
+                                    float* acc_lse, float scale, cudaStream_t stream) {
+  static bool configured = false;
+  auto kern = attn_bf16_sm100_kernel<D>;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         AttnCfg<D>::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int64_t grid = int64_t(tp.n_items) * tp.BH;
+  if (grid <= 0) return cudaSuccess;
+  kern<<<dim3(unsigned(grid)), kAttnThreads, AttnCfg<D>::kSmemBytes, stream>>>(
+      maps[0], maps[1], maps[2], tp, acc_o, acc_lse, scale * 1.4426950408889634f);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn_bf16(int D, const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
+                             float* acc_lse, float scale, cudaStream_t stream) {
+  if (D == 128) return launch_bf16_impl<128>(maps, tp, acc_o, acc_lse, scale, stream);
+  if (D == 64) return launch_bf16_impl<64>(maps, tp, acc_o, acc_lse, scale, stream);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace cqs

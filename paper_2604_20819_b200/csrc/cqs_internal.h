@@ -1,0 +1,60 @@
+// Internal declarations shared by the libcqs translation units (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/cqs.h"
+
+namespace cqs {
+
+// Thread-local error message (cqs_last_error).
+cqs_status fail(cqs_status st, const std::string& msg);
+
+struct Seg {
+  int64_t start;                 // global token id of the first token
+  int64_t len;
+  uint8_t codes[CQS_MAX_DEPTH];  // per level: index of its chunk in I order (0 = owner)
+};
+
+struct Task {
+  int32_t nseg = 0;
+  int32_t rank = -1;
+  uint64_t work = 0;
+  int64_t seg_off = 0;           // into cqs_plan::segs
+  int32_t quorum[CQS_MAX_DEPTH] = {};
+  uint32_t kept[CQS_MAX_SEGS] = {};
+};
+
+}  // namespace cqs
+
+struct cqs_plan_s {
+  cqs_plan_desc desc;                // offsets pointer re-pointed at I below
+  std::vector<int32_t> I;
+  int32_t depth = 0;
+  int32_t acc_depth = 0;             // streamed mode accumulator tier
+  int32_t n_stage_buffers = 0;
+  std::vector<cqs::Task> tasks;      // c^depth, lexicographic
+  std::vector<cqs::Seg> segs;        // CSR storage of task segments
+  std::vector<int64_t> my_order;     // non-empty tasks of `rank`, execution order
+  int64_t n_empty = 0, max_task_rows = 0, max_staged_rows = 0, max_acc_rows = 0;
+  uint64_t total_work = 0, my_work = 0;
+  uint64_t dev_ws = 0, host_ws = 0, predicted_peak = 0;
+};
+
+namespace cqs {
+// Memory model (plan.cpp).  acc_rows = rows of the device accumulator tier.
+struct MemModel {
+  uint64_t caller_dev, dev_ws, host_ws;
+};
+MemModel memory_model(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_rows,
+                      int32_t n_stage_buffers);
+uint64_t align256(uint64_t x);
+// Section offsets of the device workspace (forward.cu must follow memory_model exactly).
+struct WsLayout {
+  uint64_t acc_o, acc_lse, stage, stage_bytes_per_buf, flush, total;
+};
+WsLayout ws_layout(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_rows,
+                   int32_t n_stage_buffers);
+constexpr int64_t kFlushRows = 65536;
+}  // namespace cqs

@@ -1,0 +1,454 @@
+// CQS planner: Algorithm 3 BuildSubseq in segment form, the CQS mask
+// (P:130-134), LPT task sharding and the device-memory model used to choose the
+// divide depth from a byte budget (uniform scheduling; R14).
+//
+// Independent of oracle/: the oracle follows Alg. 3 literally on token arrays and dense masks; this
+// planner never materialises token ids.  A leaf is a list of maximal *segments* (runs of
+// consecutive global token ids whose per-level chunk codes are equal); the layout/gather steps of
+// Alg. 3 are applied to segment lists, and the mask M_i is represented by the
+// per-level codes: local pair (p,q) is masked iff at some level t both lie in the same non-owner
+// chunk (code_t(p) == code_t(q) != 0), which is exactly "zero G x G for every group G" with the
+// groups of P:295-298.  Every segment pair block is therefore wholly kept or wholly masked.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "cqs_internal.h"
+
+namespace cqs {
+
+static thread_local std::string g_err;
+
+cqs_status fail(cqs_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
+
+static int64_t elem_size(cqs_dtype t) { return t == CQS_BF16 ? 2 : 4; }
+
+WsLayout ws_layout(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_rows,
+                   int32_t n_stage_buffers) {
+  const uint64_t BH = uint64_t(d.B) * d.H, D = d.D;
+  WsLayout w{};
+  uint64_t off = 0;
+  w.acc_o = off;
+  off += align256(uint64_t(acc_rows) * BH * D * 4);
+  w.acc_lse = off;
+  off += align256(uint64_t(acc_rows) * BH * 4);
+  w.stage = off;
+  w.stage_bytes_per_buf = 0;
+  if (d.qkv_loc == CQS_LOC_PINNED_HOST) {
+    // three tensors [BH][staged_rows][D] per buffer
+    w.stage_bytes_per_buf = 3 * align256(BH * uint64_t(staged_rows) * D * elem_size(d.in_dtype));
+    off += uint64_t(n_stage_buffers) * w.stage_bytes_per_buf;
+  }
+  w.flush = off;
+  if (d.qkv_loc == CQS_LOC_PINNED_HOST || d.out_loc == CQS_LOC_PINNED_HOST) {
+    const uint64_t F = uint64_t(std::min<int64_t>(acc_rows, kFlushRows));
+    off += 2 * (align256(F * BH * D * 4) + align256(F * BH * 4));
+  }
+  w.total = off;
+  return w;
+}
+
+MemModel memory_model(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_rows,
+                      int32_t n_stage_buffers) {
+  const uint64_t BH = uint64_t(d.B) * d.H, N = d.N, D = d.D;
+  MemModel m{};
+  m.caller_dev = 0;
+  if (d.qkv_loc == CQS_LOC_DEVICE) m.caller_dev += 3 * BH * N * D * elem_size(d.in_dtype);
+  if (d.out_loc == CQS_LOC_DEVICE) m.caller_dev += BH * N * D * elem_size(d.out_dtype) + 4 * BH * N;
+  m.dev_ws = ws_layout(d, staged_rows, acc_rows, n_stage_buffers).total;
+  m.host_ws = (acc_rows < d.N) ? align256(N * BH * D * 4) + align256(N * BH * 4) : 0;
+  return m;
+}
+
+// ----- Algorithm 3 on segment lists ----------------------------------------------------------
+
+// Chunk u of a length-L sequence: the first (L mod c) chunks get ceil(L/c) tokens (R1).
+static inline void chunk_bounds(int64_t L, int c, int u, int64_t* a, int64_t* b) {
+  const int64_t q = L / c, r = L % c;
+  *a = u * q + std::min<int64_t>(u, r);
+  *b = *a + q + (u < r ? 1 : 0);
+}
+
+// Segments of the depth-`depth` subsequence selected by quorum[0..depth).
+// Returns false if more than CQS_MAX_SEGS segments arise.
+static bool build_segments(int64_t N, int c, const std::vector<int32_t>& I, const int32_t* quorum,
+                           int depth, std::vector<Seg>& out) {
+  std::vector<Seg> cur(1), nxt;
+  cur[0].start = 0;
+  cur[0].len = N;
+  std::memset(cur[0].codes, 0, sizeof(cur[0].codes));
+  for (int t = 0; t < depth; ++t) {
+    int64_t L = 0;
+    for (auto& s : cur) L += s.len;
+    nxt.clear();
+    for (size_t i = 0; i < I.size(); ++i) {              // chunks in I order (R2)
+      const int u = (quorum[t] + I[i]) % c;
+      int64_t a, b;
+      chunk_bounds(L, c, u, &a, &b);
+      int64_t pos = 0;
+      for (auto& s : cur) {                                // gather
+        const int64_t lo = std::max(a, pos), hi = std::min(b, pos + s.len);
+        if (lo < hi) {
+          Seg p = s;
+          p.start = s.start + (lo - pos);
+          p.len = hi - lo;
+          p.codes[t] = uint8_t(i);                         // label of this level
+          if (!nxt.empty()) {
+            Seg& q = nxt.back();
+            if (q.start + q.len == p.start && std::memcmp(q.codes, p.codes, t + 1) == 0) {
+              q.len += p.len;
+              pos += s.len;
+              continue;
+            }
+          }
+          nxt.push_back(p);
+        }
+        pos += s.len;
+      }
+    }
+    cur.swap(nxt);
+    if (cur.size() > CQS_MAX_SEGS) return false;
+  }
+  out = cur;
+  return true;
+}
+
+// Segment-block form of LocalMaskFromGroupRuns: masked iff some level puts both
+// segments in the same non-owner chunk.
+static inline bool kept_pair(const Seg& a, const Seg& b, int depth) {
+  for (int t = 0; t < depth; ++t)
+    if (a.codes[t] == b.codes[t] && a.codes[t] != 0) return false;
+  return true;
+}
+
+static bool is_difference_set(const std::vector<int32_t>& I, int c) {
+  std::vector<int> cnt(c, 0);
+  for (size_t i = 0; i < I.size(); ++i)
+    for (size_t j = 0; j < I.size(); ++j)
+      if (i != j) cnt[((I[i] - I[j]) % c + c) % c]++;
+  if (cnt[0] != 0) return false;
+  for (int r = 1; r < c; ++r)
+    if (cnt[r] != 1) return false;
+  return true;
+}
+
+static int64_t ipow(int64_t b, int e) {
+  int64_t r = 1;
+  while (e-- > 0) r *= b;
+  return r;
+}
+
+// Longest depth-j subsequence (rows of one accumulator subtree) — lengths only.
+static int64_t max_node_rows(int64_t N, int c, const std::vector<int32_t>& I, int j) {
+  std::vector<int64_t> lens{N}, nxt;
+  for (int t = 0; t < j; ++t) {
+    nxt.clear();
+    std::vector<int64_t> uniq(lens);
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    for (int64_t L : uniq)
+      for (int q = 0; q < c; ++q) {
+        int64_t tot = 0;
+        for (int32_t o : I) {
+          int64_t a, b;
+          chunk_bounds(L, c, (q + o) % c, &a, &b);
+          tot += b - a;
+        }
+        nxt.push_back(tot);
+      }
+    lens.swap(nxt);
+  }
+  return *std::max_element(lens.begin(), lens.end());
+}
+
+struct LeafSet {
+  std::vector<Task> tasks;
+  std::vector<Seg> segs;
+  int64_t n_empty = 0, max_rows = 0, max_staged = 0;
+  uint64_t total_work = 0;
+};
+
+static cqs_status enumerate_leaves(const cqs_plan_desc& d, const std::vector<int32_t>& I,
+                                   int depth, LeafSet& ls) {
+  const int c = d.c;
+  const int64_t n = ipow(c, depth);
+  ls.tasks.assign(size_t(n), Task{});
+  ls.segs.clear();
+  ls.segs.reserve(size_t(n) * 4);
+  std::vector<Seg> segs;
+  int32_t qt[CQS_MAX_DEPTH] = {};
+  for (int64_t idx = 0; idx < n; ++idx) {
+    int64_t r = idx;                                       // lexicographic, q_1 most significant
+    for (int t = depth - 1; t >= 0; --t) {
+      qt[t] = int32_t(r % c);
+      r /= c;
+    }
+    if (!build_segments(d.N, c, I, qt, depth, segs))
+      return fail(CQS_E_UNSUPPORTED, "task has more than CQS_MAX_SEGS segments");
+    Task& T = ls.tasks[size_t(idx)];
+    std::copy(qt, qt + depth, T.quorum);
+    T.nseg = int32_t(segs.size());
+    T.seg_off = int64_t(ls.segs.size());
+    uint32_t used = 0;
+    int64_t rows = 0;
+    for (int a = 0; a < T.nseg; ++a) {
+      rows += segs[a].len;
+      for (int b = 0; b < T.nseg; ++b)
+        if (kept_pair(segs[a], segs[b], depth)) {
+          T.kept[a] |= 1u << b;
+          T.work += uint64_t(segs[a].len) * uint64_t(segs[b].len);
+          used |= (1u << a) | (1u << b);
+        }
+    }
+    int64_t staged = 0;
+    for (int a = 0; a < T.nseg; ++a)
+      if (used & (1u << a)) staged += segs[a].len;
+    ls.segs.insert(ls.segs.end(), segs.begin(), segs.end());
+    ls.total_work += T.work;
+    if (T.work == 0) ls.n_empty++;
+    ls.max_rows = std::max(ls.max_rows, rows);
+    ls.max_staged = std::max(ls.max_staged, staged);
+  }
+  return CQS_OK;
+}
+
+}  // namespace cqs
+
+using namespace cqs;
+
+extern "C" {
+
+const char* cqs_last_error(void) { return g_err.c_str(); }
+int32_t cqs_abi_version(void) { return CQS_ABI_VERSION; }
+
+static cqs_status validate_desc(const cqs_plan_desc* d, std::vector<int32_t>& I) {
+  if (!d) return fail(CQS_E_INVALID, "desc is NULL");
+  if (d->N < 1 || d->N > INT32_MAX) return fail(CQS_E_INVALID, "N must be in [1, 2^31)");
+  if (d->B < 1 || d->H < 1 || d->D < 1) return fail(CQS_E_INVALID, "B, H, D must be >= 1");
+  if (d->l < 1 || d->c != d->l * (d->l - 1) + 1)
+    return fail(CQS_E_INVALID, "c must equal l(l-1)+1 (P:30)");
+  if (!d->offsets) return fail(CQS_E_INVALID, "offsets is NULL");
+  I.assign(d->offsets, d->offsets + d->l);
+  for (int i = 0; i < d->l; ++i) {
+    if (I[i] < 0 || I[i] >= d->c) return fail(CQS_E_INVALID, "offset out of [0, c)");
+    for (int j = 0; j < i; ++j)
+      if (I[i] == I[j]) return fail(CQS_E_INVALID, "duplicate offset");
+  }
+  if (I[0] != 0) return fail(CQS_E_INVALID, "offsets[0] must be 0 (owner chunk, R4)");
+  if (!is_difference_set(I, d->c))
+    return fail(CQS_E_INVALID, "interest set is not a (c,l,1) difference set (P:352)");
+  if (d->world < 1 || d->rank < 0 || d->rank >= d->world)
+    return fail(CQS_E_INVALID, "bad world/rank");
+  if (d->depth < -1 || d->depth >= CQS_MAX_DEPTH) return fail(CQS_E_INVALID, "bad depth");
+  if (d->depth >= 0 && d->N < ipow(d->c, d->depth))
+    return fail(CQS_E_INVALID, "N < c^depth (R10)");
+  if (d->in_dtype == CQS_BF16 && !(d->D == 64 || d->D == 128))
+    return fail(CQS_E_UNSUPPORTED, "bf16 path supports D in {64, 128}");
+  if (d->in_dtype == CQS_F32 && !(d->D % 32 == 0 && d->D <= 128))
+    return fail(CQS_E_UNSUPPORTED, "fp32 path supports D in {32, 64, 96, 128}");
+  if (d->qkv_loc == CQS_LOC_DEVICE && d->out_loc != CQS_LOC_DEVICE)
+    return fail(CQS_E_UNSUPPORTED, "resident Q/K/V require a device output");
+  return CQS_OK;
+}
+
+cqs_status cqs_memory_model(const cqs_plan_desc* desc, int32_t depth, int32_t acc_depth,
+                            int32_t n_stage_buffers, uint64_t* dev_bytes, uint64_t* host_bytes) {
+  std::vector<int32_t> I;
+  cqs_status st = validate_desc(desc, I);
+  if (st != CQS_OK) return st;
+  if (depth < 0 || acc_depth < 0 || acc_depth > depth || desc->N < ipow(desc->c, depth))
+    return fail(CQS_E_INVALID, "bad depth / acc_depth");
+  LeafSet ls;
+  int64_t staged = desc->N;
+  if (desc->qkv_loc == CQS_LOC_PINNED_HOST) {
+    if ((st = enumerate_leaves(*desc, I, depth, ls)) != CQS_OK) return st;
+    staged = ls.max_staged;
+  }
+  const int64_t acc_rows =
+      desc->qkv_loc == CQS_LOC_PINNED_HOST ? max_node_rows(desc->N, desc->c, I, acc_depth) : desc->N;
+  MemModel m = memory_model(*desc, staged, acc_rows, n_stage_buffers);
+  if (dev_bytes) *dev_bytes = m.caller_dev + m.dev_ws;
+  if (host_bytes) *host_bytes = m.host_ws;
+  return CQS_OK;
+}
+
+cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
+  if (!out) return fail(CQS_E_INVALID, "out is NULL");
+  *out = nullptr;
+  std::vector<int32_t> I;
+  cqs_status st = validate_desc(desc, I);
+  if (st != CQS_OK) return st;
+  const cqs_plan_desc& d = *desc;
+  const bool streamed = d.qkv_loc == CQS_LOC_PINNED_HOST;
+  const uint64_t budget = d.budget_bytes;
+
+  int max_depth = 0;
+  while (max_depth + 1 < CQS_MAX_DEPTH && ipow(d.c, max_depth + 1) <= d.N) ++max_depth;
+  const int k_lo = d.depth >= 0 ? d.depth : 0, k_hi = d.depth >= 0 ? d.depth : max_depth;
+
+  LeafSet ls;
+  int chosen = -1, chosen_j = 0, chosen_nbuf = 0;
+  int64_t acc_rows = d.N;
+  MemModel mm{};
+  for (int k = k_lo; k <= k_hi && chosen < 0; ++k) {
+    if ((st = enumerate_leaves(d, I, k, ls)) != CQS_OK) return st;
+    if (!streamed) {
+      mm = memory_model(d, 0, d.N, 0);
+      if (budget == 0 || mm.caller_dev + mm.dev_ws <= budget) chosen = k;
+      continue;
+    }
+    for (int nbuf = 2; nbuf >= 1 && chosen < 0; --nbuf)
+      for (int j = 0; j <= k && chosen < 0; ++j) {
+        const int64_t rows = max_node_rows(d.N, d.c, I, j);
+        MemModel m = memory_model(d, ls.max_staged, rows, nbuf);
+        if (budget == 0 || m.caller_dev + m.dev_ws <= budget) {
+          chosen = k, chosen_j = j, chosen_nbuf = nbuf, acc_rows = rows, mm = m;
+        }
+      }
+  }
+  if (chosen < 0)
+    return fail(CQS_E_INFEASIBLE, "no divide depth fits budget_bytes under the memory model");
+
+  auto* p = new cqs_plan_t();
+  p->desc = d;
+  p->I = I;
+  p->desc.offsets = p->I.data();
+  p->depth = chosen;
+  p->acc_depth = streamed ? chosen_j : 0;
+  p->n_stage_buffers = streamed ? chosen_nbuf : 0;
+  p->tasks.swap(ls.tasks);
+  p->segs.swap(ls.segs);
+  p->n_empty = ls.n_empty;
+  p->max_task_rows = ls.max_rows;
+  p->max_staged_rows = streamed ? ls.max_staged : 0;
+  p->max_acc_rows = acc_rows;
+  p->total_work = ls.total_work;
+
+  // LPT on exact work (largest first, ties by index) -> least-loaded rank (ties lowest rank).
+  std::vector<int64_t> order;
+  for (int64_t i = 0; i < int64_t(p->tasks.size()); ++i)
+    if (p->tasks[size_t(i)].work > 0) order.push_back(i);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    return p->tasks[size_t(a)].work > p->tasks[size_t(b)].work;
+  });
+  std::vector<uint64_t> load(size_t(d.world), 0);
+  for (int64_t i : order) {
+    const size_t r = size_t(std::min_element(load.begin(), load.end()) - load.begin());
+    p->tasks[size_t(i)].rank = int32_t(r);
+    load[r] += p->tasks[size_t(i)].work;
+  }
+  for (int64_t i = 0; i < int64_t(p->tasks.size()); ++i)
+    if (p->tasks[size_t(i)].rank == d.rank) {
+      p->my_order.push_back(i);
+      p->my_work += p->tasks[size_t(i)].work;
+    }
+  p->dev_ws = mm.dev_ws;
+  p->host_ws = mm.host_ws;
+  p->predicted_peak = mm.caller_dev + mm.dev_ws;
+  *out = p;
+  return CQS_OK;
+}
+
+cqs_status cqs_plan_info(const cqs_plan_t* p, cqs_plan_info_t* info) {
+  if (!p || !info) return fail(CQS_E_INVALID, "NULL argument");
+  std::memset(info, 0, sizeof(*info));
+  info->depth = p->depth;
+  info->acc_depth = p->acc_depth;
+  info->n_stage_buffers = p->n_stage_buffers;
+  info->n_tasks = int64_t(p->tasks.size());
+  info->n_empty = p->n_empty;
+  info->max_task_rows = p->max_task_rows;
+  info->max_staged_rows = p->max_staged_rows;
+  info->total_work_pairs = p->total_work;
+  info->my_tasks = int64_t(p->my_order.size());
+  info->my_work_pairs = p->my_work;
+  info->dev_workspace_bytes = p->dev_ws;
+  info->host_workspace_bytes = p->host_ws;
+  info->predicted_peak_bytes = p->predicted_peak;
+  return CQS_OK;
+}
+
+cqs_status cqs_plan_task(const cqs_plan_t* p, int64_t idx, cqs_task_t* t) {
+  if (!p || !t) return fail(CQS_E_INVALID, "NULL argument");
+  if (idx < 0 || idx >= int64_t(p->tasks.size())) return fail(CQS_E_INVALID, "task index");
+  std::memset(t, 0, sizeof(*t));
+  const Task& T = p->tasks[size_t(idx)];
+  t->nseg = T.nseg;
+  t->rank = T.rank;
+  t->work = T.work;
+  std::copy(T.quorum, T.quorum + CQS_MAX_DEPTH, t->quorum);
+  for (int a = 0; a < T.nseg; ++a) {
+    const Seg& s = p->segs[size_t(T.seg_off + a)];
+    t->seg_start[a] = s.start;
+    t->seg_len[a] = s.len;
+    std::memcpy(t->seg_codes[a], s.codes, CQS_MAX_DEPTH);
+    t->kept[a] = T.kept[a];
+  }
+  return CQS_OK;
+}
+
+cqs_status cqs_plan_serialize(const cqs_plan_t* p, void* buf, size_t* len) {
+  if (!p || !len) return fail(CQS_E_INVALID, "NULL argument");
+  std::string b;
+  auto put = [&](const void* x, size_t n) { b.append(static_cast<const char*>(x), n); };
+  const uint32_t ver = 1;
+  b.append("CQSP", 4);
+  put(&ver, 4);
+  put(&p->desc.N, 8);
+  put(&p->desc.c, 4);
+  put(&p->desc.l, 4);
+  put(p->I.data(), 4 * p->I.size());
+  put(&p->depth, 4);
+  const int64_t nt = int64_t(p->tasks.size());
+  put(&nt, 8);
+  for (const Task& T : p->tasks) {
+    put(&T.nseg, 4);
+    put(&T.work, 8);
+    for (int a = 0; a < T.nseg; ++a) {
+      const Seg& s = p->segs[size_t(T.seg_off + a)];
+      put(&s.start, 8);
+      put(&s.len, 8);
+      put(s.codes, size_t(p->depth));
+    }
+    put(T.kept, 4 * size_t(T.nseg));
+  }
+  if (!buf) {
+    *len = b.size();
+    return CQS_OK;
+  }
+  if (*len < b.size()) {
+    *len = b.size();
+    return fail(CQS_E_INVALID, "buffer too small");
+  }
+  std::memcpy(buf, b.data(), b.size());
+  *len = b.size();
+  return CQS_OK;
+}
+
+void cqs_plan_destroy(cqs_plan_t* p) { delete p; }
+
+cqs_status cqs_forward_workspace_size(const cqs_plan_t* p, size_t* dev_bytes, size_t* host_bytes) {
+  if (!p) return fail(CQS_E_INVALID, "plan is NULL");
+  if (dev_bytes) *dev_bytes = size_t(p->dev_ws);
+  if (host_bytes) *host_bytes = size_t(p->host_ws);
+  return CQS_OK;
+}
+
+cqs_status cqs_shard_rows(int64_t N, int32_t world, int32_t rank, int64_t* row0, int64_t* rows) {
+  if (world < 1 || rank < 0 || rank >= world || N < 0 || !row0 || !rows)
+    return fail(CQS_E_INVALID, "bad shard arguments");
+  const int64_t a = (N * rank) / world, b = (N * (rank + 1)) / world;
+  *row0 = a;
+  *rows = b - a;
+  return CQS_OK;
+}
+
+}  // extern "C"
