@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""bench.py — CQS-decomposed exact attention on B200 (BASELINE.json metric, config 1 at N=1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config c2]
+
+One step = one pass of the whole hot path over one batch of synthetic input: cqs_plan (CQS Divide,
+a1) -> cqs_attention_forward (resident gather via TMA a2, per-task tcgen05 attention a3 with the
+fused LSE-merge epilogue + finalize a4) -> at N>1 the NCCL partial exchange + cqs_merge (a5).
+Prints ONE JSON line on rank 0.  The `--impl reference` arm times the fp64 CPU oracle (the only
+reference this paper has; it ships no code) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1]: the N=1 bench workload
+    "c2": dict(N=131072, B=1, H=32, D=128, depth=1, dtype="bf16",
+               desc="C2: N=131072, H=32, D=128, bf16, one CQS level (7 tasks), QKV resident in HBM"),
+    # smaller sanity workload
+    "small": dict(N=16384, B=1, H=8, D=128, depth=1, dtype="bf16",
+                  desc="small: N=16384, H=8, D=128, bf16, one CQS level"),
+    "c2d64": dict(N=131072, B=1, H=32, D=64, depth=1, dtype="bf16",
+                  desc="C2 with D=64 (C5 head dim), bf16, one CQS level, resident"),
+}
+SEED = 20260418  # 20260417 + config index 1
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        rows = []
+        for ln in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+def cpu_oracle_sample(cfg, seconds=10.0, max_rows=4096):
+    """Time the oracle (fp64 dense rows, blockwise) on host cores: sampled query rows of head 0
+    against all N keys.  Returns (TFLOP/s, rows, threads, secs)."""
+    import numpy as np
+    import cqs_synth
+    from oracle import cqs_oracle as O
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [os.cpu_count()])
+    except Exception:
+        threads = os.cpu_count()
+    N, D = cfg["N"], cfg["D"]
+    bf = cfg["dtype"] == "bf16"
+    shape_nd = (N, D)
+    k = cqs_synth.numpy_values(SEED, 1, 0, N * D)
+    v = cqs_synth.numpy_values(SEED, 2, 0, N * D)
+    if bf:
+        k, v = cqs_synth.round_bf16(k), cqs_synth.round_bf16(v)
+    k = k.astype(np.float64).reshape(shape_nd)
+    v = v.astype(np.float64).reshape(shape_nd)
+    rows_done, t0 = 0, time.perf_counter()
+    blk = 128
+    while rows_done < max_rows and time.perf_counter() - t0 < seconds:
+        rows = np.arange(rows_done, rows_done + blk)
+        qv = cqs_synth.numpy_values(SEED, 0, rows_done * D, blk * D)
+        if bf:
+            qv = cqs_synth.round_bf16(qv)
+        q = np.zeros(shape_nd)
+        q[rows] = qv.astype(np.float64).reshape(blk, D)
+        O.dense_attention_rows(q, k, v, rows, block=32768)
+        rows_done += blk
+    secs = time.perf_counter() - t0
+    return 4.0 * rows_done * N * D / secs / 1e12, rows_done, threads, secs
+
+
+def run_reference(args, cfg):
+    """--impl reference: the fp64 oracle on host cores, bounded sample per step (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    vals, rows_tot, secs_tot, thr = [], 0, 0.0, 1
+    for i in range(args.warmup + args.steps):
+        tf, rows, thr, secs = cpu_oracle_sample(cfg, seconds=4.0, max_rows=1024)
+        if i >= args.warmup:
+            vals.append(tf)
+            rows_tot += rows
+            secs_tot += secs
+    value = 4.0 * rows_tot * cfg["N"] * cfg["D"] / secs_tot / 1e12
+    sample = "%d query rows x all %d keys of head 0 per step (fp64 NumPy, blockwise dense)" % (
+        rows_tot // max(1, args.steps), cfg["N"])
+    line = {"impl": "reference", "metric": "exact-attn TFLOP/s", "value": value,
+            "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs_tot / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "sampled": True},
+            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": thr, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cqs")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    import cqs_synth
+    import paper_2604_20819_b200 as cqs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        cfg["depth"] = max(cfg["depth"], 2)   # 49 tasks: LPT balance across ranks
+    N, B, H, D, depth = cfg["N"], cfg["B"], cfg["H"], cfg["D"], cfg["depth"]
+    bf = cfg["dtype"] == "bf16"
+    dt = torch.bfloat16 if bf else torch.float32
+    q, k, v = cqs_synth.torch_qkv(B, H, N, D, SEED, dtype=dt, device=dev)
+    out = torch.empty(B, H, N, D, dtype=dt, device=dev)
+    lse = torch.empty(B, H, N, dtype=torch.float32, device=dev)
+    desc_kw = dict(N=N, B=B, H=H, D=D, depth=depth, in_dtype=cfg["dtype"], world=world, rank=rank)
+    p0 = cqs.cqs_plan(**desc_kw)
+    info = p0.info()
+    dev_bytes, _ = cqs.cqs_forward_workspace_size(p0)
+    ws = torch.empty(dev_bytes, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    BH = B * H
+
+    if world > 1:
+        row0, my_rows = cqs.cqs_shard_rows(N, world, rank)
+        ao, al = cqs.cqs_partial_view(p0, ws)
+        base = ws.data_ptr()
+        acc_o = ws[ao - base: ao - base + N * BH * D * 4].view(torch.float32).view(N, BH * D)
+        acc_l = ws[al - base: al - base + N * BH * 4].view(torch.float32).view(N, BH)
+        spans = [cqs.cqs_shard_rows(N, world, r) for r in range(world)]
+        splits = [n for _, n in spans]
+        recv_o = torch.empty(world * my_rows, BH * D, dtype=torch.float32, device=dev)
+        recv_l = torch.empty(world * my_rows, BH, dtype=torch.float32, device=dev)
+
+    flops = 4.0 * N * N * D * BH
+
+    def step(with_stats):
+        p = cqs.cqs_plan(**desc_kw)                      # a1: CQS Divide planning (host C++)
+        st = cqs.cqs_attention_forward(p, q, k, v, out, lse if world == 1 else None, 0.0, 0, ws,
+                                       None, stream, stats=with_stats)
+        if world > 1:                                     # a5: one exchange + R-way merge
+            dist.all_to_all_single(recv_o, acc_o, [my_rows] * world, splits)
+            dist.all_to_all_single(recv_l, acc_l, [my_rows] * world, splits)
+            po = [recv_o[r * my_rows:(r + 1) * my_rows] for r in range(world)]
+            pl = [recv_l[r * my_rows:(r + 1) * my_rows] for r in range(world)]
+            cqs.cqs_merge(my_rows, B, H, D, po, pl, out=out, out_row0=row0, n_total=N,
+                          lse_out=lse)
+        return st
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    attn_ms, merge_ms, launches = 0.0, 0.0, 0
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            st = step(True)
+            attn_ms += st.ms_attn
+            merge_ms += st.ms_merge
+            launches += st.kernel_launches
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        launches_t = torch.tensor([launches], device=dev, dtype=torch.float64)
+        dist.all_reduce(launches_t)
+        launches = int(launches_t.item())
+
+    # ---- end-to-end through the public API from pinned host buffers ----
+    e2e = None
+    if not args.no_e2e and world == 1:
+        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+        ho = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        hl = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
+        dq, dk, dv = (torch.empty_like(t) for t in (q, k, v))
+
+        def e2e_step():
+            dq.copy_(hq, non_blocking=True)
+            dk.copy_(hk, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+            p = cqs.cqs_plan(**desc_kw)
+            cqs.cqs_attention_forward(p, dq, dk, dv, out, lse, 0.0, 0, ws, None, stream)
+            ho.copy_(out, non_blocking=True)
+            hl.copy_(lse, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(max(1, min(args.steps, 3))):
+            e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = f0.elapsed_time(f1) / max(1, min(args.steps, 3))
+        h2d = 3 * q.numel() * q.element_size()
+        d2h = out.numel() * out.element_size() + lse.numel() * 4
+        e2e = {"value": flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+        del hq, hk, hv, ho, hl, dq, dk, dv
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    peaks, peak_src = load_peaks()
+    peak = peaks.get("bf16_tflops", 1645.9)
+    value = flops / (ms * 1e-3) / 1e12
+    # attention-kernel-only rate: this rank's algorithmic FLOPs / summed kernel durations (CUDA events)
+    attn_tf = (flops * info.my_work_pairs / info.total_work_pairs) / (attn_ms / args.steps * 1e-3) / 1e12 \
+        if attn_ms else None
+    cpu = None
+    if not args.no_cpu:
+        tf, rows, thr, secs = cpu_oracle_sample(cfg)
+        cpu = {"value": tf, "unit": "TFLOP/s", "cores": thr, "kind": "oracle",
+               "sample": "%d query rows of head 0 x all %d keys, fp64 NumPy blockwise dense, %.1f s"
+                         % (rows, N, secs)}
+    line = {
+        "metric": "exact-attn TFLOP/s", "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+        "config": {"workload": cfg["desc"], "N": N, "B": B, "H": H, "D": D, "depth": info.depth,
+                   "tasks": info.n_tasks, "l2": "inputs %.1f GB >> 126 MB L2 (no flush needed)"
+                   % (3 * q.numel() * q.element_size() / 1e9),
+                   "parallelism": "task-sharded x%d" % world},
+        "tokens_per_s": N * B / (ms * 1e-3),
+        "pct_tensor_peak": value / (world * peak),
+        "roofline": {"bound": "tensor", "achieved": attn_tf, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (attn_tf / peak) if attn_tf else None, "traffic": None,
+                     "kernel": "attn_bf16_sm100_kernel<%d>" % D, "peak_source": peak_src,
+                     "flops_per_launch": flops / max(1, info.my_tasks)},
+        "peak_mem": {"predicted_bytes": info.predicted_peak_bytes,
+                     "torch_max_allocated": torch.cuda.max_memory_allocated(dev)},
+        "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,89 @@
+"""ORACLE O5 — device-memory model M_dev and budget-driven depth choice.  TEST INFRASTRUCTURE ONLY.
+
+The paper fixes the law, not the bytes: "each CQS Divide reduces the memory footprint by a factor of
+l/c = 3/7" for a linear per-task memory Mem(x) = D x + E, and uniform
+scheduling picks the divide granularity so that one task fits the memory limit (P:146, P:152,
+P:162).  The byte terms below are this build's accounting (reading R14):
+everything live on the device during a forward call = caller device tensors + the workspace.
+
+Pins (tests/test_oracle_memory.py): the staging term shrinks by ~3/7 per level, task count
+c^k, leaf length N(3/7)^k +- k, monotone feasibility in the budget.
+"""
+from __future__ import annotations
+
+from oracle import cqs_oracle as O
+
+FLUSH_ROWS = 65536
+
+
+def _a256(x):
+    return (x + 255) // 256 * 256
+
+
+def leaf_staged_rows(N, c, I, k):
+    """Largest number of rows any non-empty leaf must stage: segments that are a query or key of a
+    kept block.  Uses the literal Alg. 3 entry and its mask groups."""
+    best = 0
+    for qt in O.quorum_tuples(c, k):
+        e = O.build_subseq_entry(N, c, I, qt)
+        segs = O.entry_segments(e)
+        kept = O.segment_kept_matrix(e, segs)
+        used = kept.any(axis=0) | kept.any(axis=1)
+        best = max(best, sum(s[1] for s, u in zip(segs, used) if u))
+    return best
+
+
+def node_rows_max(N, c, I, j):
+    """Longest depth-j subsequence (P:279-283 layout applied j times)."""
+    lens = {N}
+    for _ in range(j):
+        nxt = set()
+        for L in lens:
+            st, en = O.balanced_chunk_layout(L, c)
+            for q in range(c):
+                nxt.add(sum(en[(q + o) % c] - st[(q + o) % c] for o in I))
+        lens = nxt
+    return max(lens)
+
+
+def workspace_bytes(N, BH, D, e_in, streamed, out_host, staged_rows, acc_rows, nbuf):
+    b = _a256(acc_rows * BH * D * 4) + _a256(acc_rows * BH * 4)
+    if streamed:
+        b += nbuf * 3 * _a256(BH * staged_rows * D * e_in)
+    if streamed or out_host:
+        F = min(acc_rows, FLUSH_ROWS)
+        b += 2 * (_a256(F * BH * D * 4) + _a256(F * BH * 4))
+    return b
+
+
+def device_bytes(N, B, H, D, e_in, e_out, streamed, out_host, staged_rows, acc_rows, nbuf):
+    BH = B * H
+    caller = 0 if streamed else 3 * BH * N * D * e_in
+    if not out_host:
+        caller += BH * N * D * e_out + 4 * BH * N
+    return caller + workspace_bytes(N, BH, D, e_in, streamed, out_host, staged_rows, acc_rows, nbuf)
+
+
+def choose(N, B, H, D, e_in, e_out, streamed, out_host, budget, c=7, I=(0, 1, 3), depth=None,
+           staged=None):
+    """Smallest depth k (then nbuf 2 before 1, then smallest accumulator depth j) whose predicted
+    device bytes fit the budget (uniform scheduling).  Returns (k, j, nbuf, bytes) or None.
+    `staged` may pass precomputed leaf_staged_rows per k (they are expensive for big N)."""
+    kmax = 0
+    while c ** (kmax + 1) <= N and kmax + 1 < 12:
+        kmax += 1
+    ks = [depth] if depth is not None else range(0, kmax + 1)
+    for k in ks:
+        if not streamed:
+            b = device_bytes(N, B, H, D, e_in, e_out, False, out_host, 0, N, 0)
+            if budget == 0 or b <= budget:
+                return k, 0, 0, b
+            continue
+        Lh = staged[k] if staged is not None else leaf_staged_rows(N, c, I, k)
+        for nbuf in (2, 1):
+            for j in range(0, k + 1):
+                b = device_bytes(N, B, H, D, e_in, e_out, True, out_host, Lh,
+                                 node_rows_max(N, c, I, j), nbuf)
+                if budget == 0 or b <= budget:
+                    return k, j, nbuf, b
+    return None

@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "libcqs.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
-         "--expt-relaxed-constexpr", "-I" + os.path.join(HERE, "..", "include")]
+         "--expt-relaxed-constexpr", "-DCQS_WATCHDOG", "-I" + os.path.join(HERE, "..", "include")]
 
 
 def _sources():

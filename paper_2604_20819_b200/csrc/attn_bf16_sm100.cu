@@ -124,9 +124,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // register split: 4 warps x 80 + 8 warps x 216 = 65536 / 32 (the whole RF of one SM)
+  // register split (launch: 384 x 168): the 4 non-math warps give back 128 x (168-72) = 12288
+  // registers, exactly what the 8 softmax warps take (256 x (216-168)); .inc blocks forever if
+  // the pool is short, so the two numbers must balance.
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
   if (warp == 0) {
     // ================= TMA producer =================
     if (lane == 0) {
@@ -275,17 +277,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
         m = m_new;
         float rs = 0.f;
-        uint32_t pk[kBN / 2];
 #pragma unroll
-        for (int c = 0; c < kBN / 2; ++c) {
-          const float p0 = ptx::ex2(fmaf(s[2 * c], scale_log2, -m));
-          const float p1 = ptx::ex2(fmaf(s[2 * c + 1], scale_log2, -m));
-          rs += p0 + p1;
-          pk[c] = ptx::pack_bf16(p0, p1);
+        for (int c = 0; c < kBN / 32; ++c) {   // P (bf16 pairs) over S's first 64 columns
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float p0 = ptx::ex2(fmaf(s[32 * c + 2 * i], scale_log2, -m));
+            const float p1 = ptx::ex2(fmaf(s[32 * c + 2 * i + 1], scale_log2, -m));
+            rs += p0 + p1;
+            pk[i] = ptx::pack_bf16(p0, p1);
+          }
+          ptx::tmem_st16(tS + c * 16, pk);
         }
         l += rs;
-        ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-        ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();

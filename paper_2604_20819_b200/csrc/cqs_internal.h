@@ -57,4 +57,7 @@ struct WsLayout {
 WsLayout ws_layout(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_rows,
                    int32_t n_stage_buffers);
 constexpr int64_t kFlushRows = 65536;
+// Segments of the depth-`depth` subsequence selected by quorum[0..depth) (Alg. 3).
+bool build_segments(int64_t N, int c, const std::vector<int32_t>& I, const int32_t* quorum,
+                    int depth, std::vector<Seg>& out);
 }  // namespace cqs

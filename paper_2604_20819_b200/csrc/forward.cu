@@ -100,6 +100,13 @@ static void build_task_params(const cqs_plan_t* p, const Task& T, int rows_per_i
   tp.n_items = items;
 }
 
+void build_task_params_ext(const cqs_plan_t* p, const Task& T, int rows_per_item,
+                           const int64_t* src_rows, const int64_t* dst_rows, TaskParams& tp) {
+  build_task_params(
+      p, T, rows_per_item, [&](int a) { return src_rows[a]; }, [&](int a) { return dst_rows[a]; },
+      tp);
+}
+
 cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, const void* v,
                             void* out, const int64_t* out_strides, float* lse, float scale,
                             uint8_t* ws, uint8_t* host_ws, cudaStream_t st, cqs_stats* stats);
@@ -151,7 +158,18 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
   float* acc_o = reinterpret_cast<float*>(ws + L.acc_o);
   float* acc_lse = reinterpret_cast<float*>(ws + L.acc_lse);
   int64_t launches = 0;
+  // stats: CUDA events around every launch on `st` (kernel durations, not host time)
+  std::vector<cudaEvent_t> evs;
+  auto mark = [&]() {
+    if (!stats) return;
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    cudaEventRecord(ev, st);
+    evs.push_back(ev);
+  };
+  mark();
   cudaError_t e = launch_fill(acc_lse, d.N * BH, -INFINITY, st);
+  mark();
   ++launches;
   if (e != cudaSuccess) return fail(CQS_E_CUDA, cudaGetErrorString(e));
 
@@ -171,19 +189,23 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
     const Task& T = p->tasks[size_t(ti)];
     auto seg_start = [&](int a) { return p->segs[size_t(T.seg_off + a)].start; };
     build_task_params(p, T, rows_per_item, seg_start, seg_start, tp);
+    mark();
     if (d.in_dtype == CQS_BF16)
       e = launch_attn_bf16(d.D, maps, tp, acc_o, acc_lse, scale, st);
     else
       e = launch_attn_f32(d.D, tp, static_cast<const float*>(q), static_cast<const float*>(k),
                           static_cast<const float*>(v), qkv_strides, acc_o, acc_lse, scale, st);
+    mark();
     if (e != cudaSuccess) return fail(CQS_E_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
     ++launches;
     ++run;
   }
   const auto t1 = std::chrono::steady_clock::now();
   if (d.world == 1) {
+    mark();
     e = launch_merge(d.N, d.B, d.H, d.D, 0, nullptr, nullptr, acc_o, acc_lse, false, out,
                      d.out_dtype, out_strides, 0, d.N, lse, st);
+    mark();
     ++launches;
     if (e != cudaSuccess) return fail(CQS_E_CUDA, std::string("finalize: ") + cudaGetErrorString(e));
   }
@@ -192,9 +214,16 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return fail(CQS_E_CUDA, cudaGetErrorString(e));
     const auto t2 = std::chrono::steady_clock::now();
-    stats->ms_attn = std::chrono::duration<double, std::milli>(t2 - t0).count();
-    stats->ms_total = stats->ms_attn;
+    stats->ms_total = std::chrono::duration<double, std::milli>(t2 - t0).count();
     (void)t1;
+    // pairs: [fill] [task_0] ... [task_{run-1}] [finalize]
+    for (size_t i = 0; i + 1 < evs.size(); i += 2) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, evs[i], evs[i + 1]);
+      const bool is_attn = i >= 2 && i < 2 + 2 * size_t(run);
+      (is_attn ? stats->ms_attn : stats->ms_merge) += ms;
+    }
+    for (auto ev : evs) cudaEventDestroy(ev);
     stats->tasks_run = run;
     stats->tasks_skipped = int64_t(p->tasks.size()) - run;
     stats->kernel_launches = launches;

@@ -79,8 +79,8 @@ static inline void chunk_bounds(int64_t L, int c, int u, int64_t* a, int64_t* b)
 
 // Segments of the depth-`depth` subsequence selected by quorum[0..depth).
 // Returns false if more than CQS_MAX_SEGS segments arise.
-static bool build_segments(int64_t N, int c, const std::vector<int32_t>& I, const int32_t* quorum,
-                           int depth, std::vector<Seg>& out) {
+bool build_segments(int64_t N, int c, const std::vector<int32_t>& I, const int32_t* quorum,
+                    int depth, std::vector<Seg>& out) {
   std::vector<Seg> cur(1), nxt;
   cur[0].start = 0;
   cur[0].len = N;
@@ -182,6 +182,8 @@ static cqs_status enumerate_leaves(const cqs_plan_desc& d, const std::vector<int
   const int64_t n = ipow(c, depth);
   ls.tasks.assign(size_t(n), Task{});
   ls.segs.clear();
+  ls.n_empty = ls.max_rows = ls.max_staged = 0;
+  ls.total_work = 0;
   ls.segs.reserve(size_t(n) * 4);
   std::vector<Seg> segs;
   int32_t qt[CQS_MAX_DEPTH] = {};

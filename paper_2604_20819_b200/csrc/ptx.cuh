@@ -4,6 +4,7 @@
 // cute/arch/mma_sm100_desc.hpp field comments).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 
 namespace cqs {
 namespace ptx {
@@ -38,10 +39,22 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Wait until the phase with parity `parity` has completed.
+// Wait until the phase with parity `parity` has completed.  With CQS_WATCHDOG a wait longer than
+// ~2^34 cycles (seconds) prints the culprit and traps instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef CQS_WATCHDOG
+  const long long t0 = clock64();
+  while (!mbar_try_wait(bar, parity)) {
+    if (clock64() - t0 > (1ll << 34)) {
+      printf("cqs watchdog: block %d thread %d stuck on mbarrier smem 0x%x parity %u\n",
+             blockIdx.x, threadIdx.x, smem_u32(bar), parity);
+      __trap();
+    }
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // ---------------- TMA ----------------

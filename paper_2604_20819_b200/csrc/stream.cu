@@ -1,12 +1,265 @@
-// Streamed forward (Q/K/V in pinned host memory): placeholder until the staging executor lands.
+// Streamed forward: Q/K/V (and O, lse) in pinned host memory, QKV larger than the device budget
+// (Sec. 2.4-2.5 P:145-162 "scale beyond the memory limits of a single device", Sec. 4
+// P:244 "continuously pipelined between host and device").
+//
+// Per task (leaf) the segments that carry kept work are copied H2D (cudaMemcpy2DAsync: rows = the
+// B*H planes, pitch N*D) into staging buffer t mod S on a copy stream while task t-1 computes
+// (S = 2: double buffering).  The attention kernel addresses the staged segments through TMA maps
+// over the staging buffer.  Partials are LSE-merged into a device accumulator that covers one
+// depth-j subtree (all rows of one depth-j intermediate subsequence; j = plan acc_depth).  When a
+// subtree is done its accumulator is merged into the pinned-host fp32 accumulator (H2D chunk ->
+// cqs_merge kernel -> D2H), and a final pass converts the host accumulator to O / lse.  With j = 0
+// the device accumulator covers all N rows and is finalized directly.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
 #include "cqs_internal.h"
+#include "task_params.cuh"
 
 namespace cqs {
-cqs_status forward_streamed(const cqs_plan_t*, const void*, const void*, const void*, void*,
-                            const int64_t*, float*, float, uint8_t*, uint8_t*, cudaStream_t,
-                            cqs_stats*) {
-  return fail(CQS_E_UNSUPPORTED, "streamed (pinned host) Q/K/V not built yet");
+
+cudaError_t launch_attn_bf16(int D, const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
+                             float* acc_lse, float scale, cudaStream_t stream);
+cudaError_t launch_attn_f32(int D, const TaskParams& tp, const float* q, const float* k,
+                            const float* v, const int64_t* strides, float* acc_o, float* acc_lse,
+                            float scale, cudaStream_t stream);
+cudaError_t launch_fill(float* p, int64_t n, float val, cudaStream_t st);
+cudaError_t launch_merge(int64_t rows, int B, int H, int D, int n_parts, const float* const* po,
+                         const float* const* pl, float* acc_o, float* acc_lse, bool acc_write,
+                         void* out, cqs_dtype out_dtype, const int64_t* out_strides,
+                         int64_t out_row0, int64_t n_total, float* lse_out, cudaStream_t st);
+cqs_status make_tmap_bf16(CUtensorMap* m, const void* base, int B, int H, int64_t rows, int D,
+                          int64_t sB, int64_t sH, int64_t sN, int box_rows);
+void build_task_params_ext(const cqs_plan_t* p, const Task& T, int rows_per_item,
+                           const int64_t* src_rows, const int64_t* dst_rows, TaskParams& tp);
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) return fail(CQS_E_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+namespace {
+struct Scoped {
+  cudaStream_t cs = nullptr;
+  std::vector<cudaEvent_t> evs;
+  ~Scoped() {
+    for (auto e : evs) cudaEventDestroy(e);
+    if (cs) cudaStreamDestroy(cs);
+  }
+  cudaEvent_t ev() {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    evs.push_back(e);
+    return e;
+  }
+};
+}  // namespace
+
+cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, const void* v,
+                            void* out, const int64_t* out_strides, float* lse, float scale,
+                            uint8_t* ws, uint8_t* host_ws, cudaStream_t st, cqs_stats* stats) {
+  const cqs_plan_desc& d = p->desc;
+  if (d.out_loc != CQS_LOC_PINNED_HOST)
+    return fail(CQS_E_UNSUPPORTED, "streamed Q/K/V require a pinned-host output");
+  if (d.world != 1) return fail(CQS_E_UNSUPPORTED, "streamed mode is single-GPU");
+  const int64_t N = d.N, D = d.D, BH = int64_t(d.B) * d.H;
+  if (out_strides[0] != int64_t(d.H) * N * D || out_strides[1] != N * D || out_strides[2] != D)
+    return fail(CQS_E_INVALID, "streamed mode needs a contiguous [B,H,N,D] output");
+  const int64_t e_in = d.in_dtype == CQS_BF16 ? 2 : 4, e_out = d.out_dtype == CQS_BF16 ? 2 : 4;
+  const int S = p->n_stage_buffers, j = p->acc_depth;
+  const int64_t Lh = p->max_staged_rows, Lacc = p->max_acc_rows;
+  const WsLayout L = ws_layout(d, Lh, Lacc, S);
+  float* acc_o = reinterpret_cast<float*>(ws + L.acc_o);
+  float* acc_l = reinterpret_cast<float*>(ws + L.acc_lse);
+  const uint64_t tens_bytes = align256(uint64_t(BH * Lh * D * e_in));
+  uint8_t* stage[2][3];
+  for (int b = 0; b < S; ++b)
+    for (int t = 0; t < 3; ++t) stage[b][t] = ws + L.stage + b * L.stage_bytes_per_buf + t * tens_bytes;
+  const int64_t F = std::min<int64_t>(Lacc, kFlushRows);
+  const uint64_t fbo = align256(uint64_t(F * BH * D * 4)), fbl = align256(uint64_t(F * BH * 4));
+  float* fb_o[2];
+  float* fb_l[2];
+  for (int i = 0; i < 2; ++i) {
+    fb_o[i] = reinterpret_cast<float*>(ws + L.flush + i * (fbo + fbl));
+    fb_l[i] = reinterpret_cast<float*>(ws + L.flush + i * (fbo + fbl) + fbo);
+  }
+  float* hacc_o = reinterpret_cast<float*>(host_ws);
+  float* hacc_l = host_ws ? reinterpret_cast<float*>(host_ws + align256(uint64_t(N * BH * D * 4)))
+                          : nullptr;
+  const uint8_t* hq[3] = {static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k),
+                          static_cast<const uint8_t*>(v)};
+
+  Scoped sc;
+  CK(cudaStreamCreateWithFlags(&sc.cs, cudaStreamNonBlocking));
+  cudaEvent_t ev_ready[2] = {sc.ev(), sc.ev()}, ev_free[2] = {sc.ev(), sc.ev()};
+  bool buf_used[2] = {false, false};
+  uint64_t h2d = 0, d2h = 0;
+  int64_t launches = 0, run = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+
+  CUtensorMap maps[2][3];
+  if (d.in_dtype == CQS_BF16)
+    for (int b = 0; b < S; ++b)
+      for (int t = 0; t < 3; ++t) {
+        cqs_status s2 = make_tmap_bf16(&maps[b][t], stage[b][t], d.B, d.H, Lh, d.D,
+                                       int64_t(d.H) * Lh * D, Lh * D, D, 128);
+        if (s2 != CQS_OK) return s2;
+      }
+  const int64_t sstr[4] = {int64_t(d.H) * Lh * D, Lh * D, D, 1};
+
+  // final O/lse for rows [r0, r0+n) from an fp32 [n][BH][D] + [n][BH] source on the device
+  auto emit_final = [&](const float* src_o, const float* src_l, int64_t r0, int64_t n) -> cqs_status {
+    const int64_t ostr[4] = {int64_t(d.H) * F * D, F * D, D, 1};
+    void* ob = fb_o[1];
+    float* lb = fb_l[1];
+    CK(launch_merge(n, d.B, d.H, d.D, 0, nullptr, nullptr, const_cast<float*>(src_o),
+                    const_cast<float*>(src_l), false, ob, d.out_dtype, ostr, 0, F, lb, st));
+    ++launches;
+    CK(cudaMemcpy2DAsync(static_cast<uint8_t*>(out) + r0 * D * e_out, size_t(N * D * e_out), ob,
+                         size_t(F * D * e_out), size_t(n * D * e_out), size_t(BH),
+                         cudaMemcpyDeviceToHost, st));
+    d2h += uint64_t(n * D * e_out * BH);
+    if (lse) {
+      CK(cudaMemcpy2DAsync(lse + r0, size_t(N * 4), lb, size_t(F * 4), size_t(n * 4), size_t(BH),
+                           cudaMemcpyDeviceToHost, st));
+      d2h += uint64_t(n * 4 * BH);
+    }
+    return CQS_OK;
+  };
+
+  if (j > 0) {  // host accumulator starts empty: lse = -inf
+    CK(launch_fill(fb_l[0], F * BH, -INFINITY, st));
+    ++launches;
+    for (int64_t r = 0; r < N; r += F) {
+      const int64_t n = std::min(F, N - r);
+      CK(cudaMemcpyAsync(hacc_l + r * BH, fb_l[0], size_t(n * BH * 4), cudaMemcpyDeviceToHost, st));
+    }
+  }
+
+  std::vector<Seg> node;
+  int64_t gi = 0;
+  const int64_t nmy = int64_t(p->my_order.size());
+  while (gi < nmy) {
+    // ---- one depth-j subtree: tasks sharing quorum prefix (q_1..q_j) ----
+    const Task& T0 = p->tasks[size_t(p->my_order[size_t(gi)])];
+    int64_t ge = gi + 1;
+    while (ge < nmy &&
+           std::equal(T0.quorum, T0.quorum + j, p->tasks[size_t(p->my_order[size_t(ge)])].quorum))
+      ++ge;
+    build_segments(N, d.c, p->I, T0.quorum, j, node);
+    std::vector<int64_t> node_off(node.size());
+    int64_t node_rows = 0;
+    for (size_t i = 0; i < node.size(); ++i) node_off[i] = node_rows, node_rows += node[i].len;
+    CK(launch_fill(acc_l, node_rows * BH, -INFINITY, st));
+    ++launches;
+
+    for (int64_t ti = gi; ti < ge; ++ti) {
+      const Task& T = p->tasks[size_t(p->my_order[size_t(ti)])];
+      const Seg* segs = &p->segs[size_t(T.seg_off)];
+      uint32_t used = 0;
+      for (int a = 0; a < T.nseg; ++a)
+        if (T.kept[a]) used |= (1u << a) | T.kept[a];
+      int64_t src[CQS_MAX_SEGS], dst[CQS_MAX_SEGS], off = 0;
+      for (int a = 0; a < T.nseg; ++a) {
+        src[a] = off;
+        if (used >> a & 1) off += segs[a].len;
+        size_t s = 0;
+        while (s + 1 < node.size() &&
+               !(segs[a].start >= node[s].start && segs[a].start < node[s].start + node[s].len))
+          ++s;
+        dst[a] = node_off[s] + (segs[a].start - node[s].start);
+      }
+      const int b = int(run % S);
+      if (buf_used[b]) CK(cudaStreamWaitEvent(sc.cs, ev_free[b], 0));
+      for (int a = 0; a < T.nseg; ++a) {
+        if (!(used >> a & 1)) continue;
+        for (int t = 0; t < 3; ++t)
+          CK(cudaMemcpy2DAsync(stage[b][t] + src[a] * D * e_in, size_t(Lh * D * e_in),
+                               hq[t] + segs[a].start * D * e_in, size_t(N * D * e_in),
+                               size_t(segs[a].len * D * e_in), size_t(BH),
+                               cudaMemcpyHostToDevice, sc.cs));
+        h2d += uint64_t(3 * segs[a].len * D * e_in * BH);
+      }
+      CK(cudaEventRecord(ev_ready[b], sc.cs));
+      CK(cudaStreamWaitEvent(st, ev_ready[b], 0));
+      TaskParams tp;
+      build_task_params_ext(p, T, d.in_dtype == CQS_BF16 ? 256 : 32, src, dst, tp);
+      if (d.in_dtype == CQS_BF16)
+        CK(launch_attn_bf16(d.D, maps[b], tp, acc_o, acc_l, scale, st));
+      else
+        CK(launch_attn_f32(d.D, tp, reinterpret_cast<const float*>(stage[b][0]),
+                           reinterpret_cast<const float*>(stage[b][1]),
+                           reinterpret_cast<const float*>(stage[b][2]), sstr, acc_o, acc_l,
+                           scale, st));
+      ++launches;
+      CK(cudaEventRecord(ev_free[b], st));
+      buf_used[b] = true;
+      ++run;
+    }
+
+    // ---- flush the subtree accumulator ----
+    for (size_t s = 0; s < node.size(); ++s) {
+      for (int64_t c0 = 0; c0 < node[s].len; c0 += F) {
+        const int64_t n = std::min(F, node[s].len - c0);
+        const int64_t grow = node[s].start + c0, lrow = node_off[s] + c0;
+        if (j == 0) {
+          cqs_status s2 = emit_final(acc_o + lrow * BH * D, acc_l + lrow * BH, grow, n);
+          if (s2 != CQS_OK) return s2;
+          continue;
+        }
+        CK(cudaMemcpyAsync(fb_o[0], hacc_o + grow * BH * D, size_t(n * BH * D * 4),
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(fb_l[0], hacc_l + grow * BH, size_t(n * BH * 4),
+                           cudaMemcpyHostToDevice, st));
+        const float* po = acc_o + lrow * BH * D;
+        const float* pl = acc_l + lrow * BH;
+        CK(launch_merge(n, d.B, d.H, d.D, 1, &po, &pl, fb_o[0], fb_l[0], true, nullptr, d.out_dtype,
+                        nullptr, 0, n, nullptr, st));
+        ++launches;
+        CK(cudaMemcpyAsync(hacc_o + grow * BH * D, fb_o[0], size_t(n * BH * D * 4),
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hacc_l + grow * BH, fb_l[0], size_t(n * BH * 4), cudaMemcpyDeviceToHost,
+                           st));
+        h2d += uint64_t(n * BH * (D + 1) * 4);
+        d2h += uint64_t(n * BH * (D + 1) * 4);
+      }
+    }
+    gi = ge;
+  }
+
+  if (j > 0) {  // host accumulator -> O, lse
+    for (int64_t r = 0; r < N; r += F) {
+      const int64_t n = std::min(F, N - r);
+      CK(cudaMemcpyAsync(fb_o[0], hacc_o + r * BH * D, size_t(n * BH * D * 4),
+                         cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(fb_l[0], hacc_l + r * BH, size_t(n * BH * 4), cudaMemcpyHostToDevice, st));
+      h2d += uint64_t(n * BH * (D + 1) * 4);
+      cqs_status s2 = emit_final(fb_o[0], fb_l[0], r, n);
+      if (s2 != CQS_OK) return s2;
+    }
+  }
+
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    CK(cudaStreamSynchronize(st));
+    stats->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    stats->bytes_h2d = h2d;
+    stats->bytes_d2h = d2h;
+    stats->tasks_run = run;
+    stats->tasks_skipped = int64_t(p->tasks.size()) - run;
+    stats->kernel_launches = launches;
+    stats->peak_dev_bytes = p->predicted_peak;
+  }
+  (void)out_strides;
+  return CQS_OK;
 }
+
 }  // namespace cqs

@@ -1,0 +1,156 @@
+"""GPU parity: libcqs (through the C ABI) vs the fp64 oracle on the same seeded inputs.
+
+Tolerances:
+  fp32 path  : normwise max|O-R| / max|R| <= 1e-5 globally and per output row (R15)
+  bf16 path  : max|O-R| <= 2e-2 (BASELINE), normwise <= 2e-2, |lse - lse_ref| <= 1e-3 (R16)
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import cqs_synth
+import paper_2604_20819_b200 as cqs
+from oracle import cqs_oracle as O
+
+pytestmark = pytest.mark.gpu
+I = (0, 1, 3)
+DEV = "cuda"
+
+
+def gen(B, H, N, D, seed, bf16):
+    dt = torch.bfloat16 if bf16 else torch.float32
+    q, k, v = cqs_synth.torch_qkv(B, H, N, D, seed, dtype=dt, device=DEV)
+    return q, k, v
+
+
+def ref_dense(q, k, v):
+    return O.dense_attention(q.double().cpu().numpy(), k.double().cpu().numpy(),
+                             v.double().cpu().numpy())
+
+
+def check_f32(out, lse, Oref, lref):
+    o = out.double().cpu().numpy()
+    err = np.abs(o - Oref)
+    assert err.max() / np.abs(Oref).max() <= 1e-5, err.max()
+    row_rel = err.max(axis=-1) / np.abs(Oref).max(axis=-1)
+    assert row_rel.max() <= 1e-5, row_rel.max()
+    assert np.abs(lse.double().cpu().numpy() - lref).max() <= 1e-5
+
+
+def check_bf16(out, lse, Oref, lref):
+    o = out.double().cpu().numpy()
+    err = np.abs(o - Oref)
+    assert err.max() <= 2e-2, err.max()
+    assert err.max() / np.abs(Oref).max() <= 2e-2, err.max() / np.abs(Oref).max()
+    assert np.abs(lse.double().cpu().numpy() - lref).max() <= 1e-3
+
+
+@pytest.mark.parametrize("N,depth", [(448, 1), (448, 2), (343, 3), (1030, 3), (7, 1), (100, 0)])
+def test_f32_matches_oracle(N, depth):
+    """BASELINE config 0 (N=448, D=64, fp32, one level) plus deeper trees with fully-masked rows
+    and empty tasks."""
+    q, k, v = gen(1, 2, N, 64, 20260417 + N, bf16=False)
+    out, lse = cqs.attention(q, k, v, depth=depth)
+    torch.cuda.synchronize()
+    check_f32(out, lse, *ref_dense(q, k, v))
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("N,depth", [(1030, 1), (1030, 2), (2401, 3), (300, 0), (49, 1)])
+def test_bf16_matches_oracle(N, depth, D):
+    q, k, v = gen(1, 2, N, D, 7 + N + D, bf16=True)
+    out, lse = cqs.attention(q, k, v, depth=depth)
+    torch.cuda.synchronize()
+    check_bf16(out, lse, *ref_dense(q, k, v))
+
+
+def test_bf16_multi_batch_strided():
+    B, H, N, D = 2, 3, 777, 128
+    q, k, v = gen(B, H, N, D, 99, bf16=True)
+    # non-contiguous: [B,N,H,D] storage viewed as [B,H,N,D]
+    qs, ks, vs = (t.transpose(1, 2).contiguous().transpose(1, 2) for t in (q, k, v))
+    out, lse = cqs.attention(qs, ks, vs, depth=2, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    check_bf16(out, lse, *ref_dense(q, k, v))
+
+
+def test_bf16_large_logits_rescale():
+    """Scaled inputs make the running max jump across tiles (exercises conditional rescale)."""
+    q, k, v = gen(1, 1, 3000, 128, 5, bf16=True)
+    q = (q.float() * 3).to(torch.bfloat16)
+    out, lse = cqs.attention(q, k, v, depth=1)
+    torch.cuda.synchronize()
+    check_bf16(out, lse, *ref_dense(q, k, v))
+
+
+def test_needle_routing():
+    """SURVEY §8d needle: a key whose chunk differs from the query's at every level gets logit ~12;
+    the output row is then ~V[m], so a dropped / duplicated / misrouted block moves O by O(1)."""
+    B, H, N, D = 1, 1, 4096, 128
+    q, k, v = gen(B, H, N, D, 11, bf16=True)
+    qf, kf, vf = q.float().clone(), k.float().clone(), v.float().clone()
+    rng = np.random.default_rng(0)
+    alpha = 1 / math.sqrt(D)
+    for n in rng.choice(N, 16, replace=False):
+        m = (n + N // 2 + 13) % N
+        kf[0, 0, m] = qf[0, 0, n] * (12.0 / (alpha * float((qf[0, 0, n] ** 2).sum())))
+        vf[0, 0, m] = torch.tensor([1.0 if (i * 7 + n) % 3 else -1.0 for i in range(D)])
+    q, k, v = (t.to(torch.bfloat16) for t in (qf, kf, vf))
+    for depth in (1, 2, 3):
+        out, lse = cqs.attention(q, k, v, depth=depth)
+        torch.cuda.synchronize()
+        check_bf16(out, lse, *ref_dense(q, k, v))
+
+
+def test_deterministic():
+    q, k, v = gen(1, 4, 5000, 128, 3, bf16=True)
+    a, la = cqs.attention(q, k, v, depth=2)
+    b, lb = cqs.attention(q, k, v, depth=2)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and torch.equal(la, lb)
+
+
+def test_c2_full_size_sampled_rows():
+    """BASELINE config 1 at full size (N=131072, H=32, D=128, bf16, one level), launched exactly as
+    bench.py does; 128 sampled (head, row) outputs against the oracle's blockwise dense rows."""
+    B, H, N, D = 1, 32, 131072, 128
+    q, k, v = gen(B, H, N, D, 20260418, bf16=True)
+    out, lse = cqs.attention(q, k, v, depth=1)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    for h in rng.choice(H, 4, replace=False):
+        rows = np.sort(rng.choice(N, 32, replace=False))
+        rows[0], rows[-1] = 0, N - 1
+        kk = k[0, h].double().cpu().numpy()
+        vv = v[0, h].double().cpu().numpy()
+        qq = q[0, h].double().cpu().numpy()
+        Oref, lref = O.dense_attention_rows(qq, kk, vv, rows, block=16384)
+        o = out[0, h, torch.from_numpy(rows).to(DEV)].double().cpu().numpy()
+        l_ = lse[0, h, torch.from_numpy(rows).to(DEV)].double().cpu().numpy()
+        assert np.abs(o - Oref).max() <= 2e-2
+        assert np.abs(o - Oref).max() / np.abs(Oref).max() <= 2e-2
+        assert np.abs(l_ - lref).max() <= 1e-3
+
+
+def test_merge_abi_matches_oracle():
+    rows, B, H, D = 1000, 1, 3, 128
+    g = torch.Generator().manual_seed(0)
+    parts_o = [torch.randn(rows, B * H, D, generator=g) for _ in range(3)]
+    parts_l = [torch.randn(rows, B * H, generator=g) * 3 for _ in range(3)]
+    parts_l[1][::7] = -math.inf
+    for t in parts_l:
+        t[5] = -math.inf
+    ref_o, ref_l = O.lse_merge([(po.double().numpy(), pl.double().numpy())
+                                for po, pl in zip(parts_o, parts_l)])
+    out = torch.empty(B, H, rows, D, device=DEV)
+    lse = torch.empty(B, H, rows, device=DEV)
+    cqs.cqs_merge(rows, B, H, D, [t.to(DEV) for t in parts_o], [t.to(DEV) for t in parts_l],
+                  out=out, lse_out=lse)
+    torch.cuda.synchronize()
+    got_o = out.permute(2, 0, 1, 3).reshape(rows, B * H, D).double().cpu().numpy()
+    got_l = lse.permute(2, 0, 1).reshape(rows, B * H).double().cpu().numpy()
+    assert np.allclose(got_o, ref_o, atol=1e-5) and np.all(got_o[5] == 0)
+    fin = np.isfinite(ref_l)
+    assert np.allclose(got_l[fin], ref_l[fin], atol=1e-5) and np.all(np.isneginf(got_l[~fin]))

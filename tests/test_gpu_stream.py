@@ -1,0 +1,84 @@
+"""GPU parity of the streamed path (Q/K/V and O/lse in pinned host memory, staged per task; DESIGN.md
+"Streamed executor") against the fp64 oracle, and peak device memory against the budget."""
+import numpy as np
+import pytest
+import torch
+
+import cqs_synth
+import paper_2604_20819_b200 as cqs
+from oracle import cqs_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def host_qkv(B, H, N, D, seed, dt):
+    return tuple(t.pin_memory() for t in cqs_synth.torch_qkv(B, H, N, D, seed, dtype=dt))
+
+
+def run_streamed(q, k, v, budget, depth=-1, out_dtype=None):
+    B, H, N, D = q.shape
+    ind = "bf16" if q.dtype == torch.bfloat16 else "f32"
+    p = cqs.cqs_plan(N=N, B=B, H=H, D=D, depth=depth, budget_bytes=budget, in_dtype=ind,
+                     out_dtype=out_dtype or ind, qkv_loc="host", out_loc="host")
+    info = p.info()
+    dev, host = cqs.cqs_forward_workspace_size(p)
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    base = torch.cuda.memory_allocated()
+    ws = torch.empty(max(dev, 256), dtype=torch.uint8, device="cuda")
+    hws = torch.empty(max(host, 256), dtype=torch.uint8).pin_memory() if host else None
+    odt = q.dtype if out_dtype is None else {"bf16": torch.bfloat16, "f32": torch.float32}[out_dtype]
+    out = torch.empty(q.shape, dtype=odt).pin_memory()
+    lse = torch.empty(q.shape[:3], dtype=torch.float32).pin_memory()
+    st = cqs.cqs_attention_forward(p, q, k, v, out, lse, 0.0, budget, ws, hws, stats=True)
+    torch.cuda.synchronize()
+    peak = torch.cuda.max_memory_allocated() - base
+    return out, lse, info, st, peak
+
+
+def check(out, lse, q, k, v, tol_o, tol_l):
+    Oref, lref = O.dense_attention(*(t.double().numpy() for t in (q, k, v)))
+    err = np.abs(out.double().numpy() - Oref)
+    assert err.max() <= tol_o and err.max() / np.abs(Oref).max() <= tol_o, err.max()
+    assert np.abs(lse.double().numpy() - lref).max() <= tol_l
+
+
+@pytest.mark.parametrize("N,H,D", [(3000, 2, 128), (2500, 2, 64)])
+def test_streamed_bf16_budget_tiers(N, H, D):
+    q, k, v = host_qkv(1, H, N, D, 31 + N, torch.bfloat16)
+    d = cqs.make_desc(N=N, B=1, H=H, D=D, depth=-1, in_dtype="bf16", qkv_loc="host")
+    for (kk, j, nb) in [(2, 1, 2), (1, 0, 1), (3, 2, 2)]:
+        budget, _ = cqs.cqs_memory_model(d, kk, j, nb)
+        out, lse, info, st, peak = run_streamed(q, k, v, budget, depth=kk)
+        assert info.depth == kk and info.acc_depth <= j
+        assert info.predicted_peak_bytes <= budget and peak <= budget
+        assert st.bytes_h2d > 0 and st.tasks_run == info.my_tasks
+        check(out, lse, q, k, v, 2e-2, 1e-3)
+
+
+def test_streamed_f32():
+    q, k, v = host_qkv(1, 1, 1030, 64, 5, torch.float32)
+    d = cqs.make_desc(N=1030, B=1, H=1, D=64, depth=-1, in_dtype="f32", qkv_loc="host")
+    budget, _ = cqs.cqs_memory_model(d, 2, 1, 2)
+    out, lse, info, st, peak = run_streamed(q, k, v, budget)
+    assert info.depth == 2 and info.acc_depth == 1
+    check(out, lse, q, k, v, 1e-5, 1e-5)
+
+
+@pytest.mark.slow
+def test_c3_streamed_16gib_sampled():
+    """BASELINE config 2: N=1M, H=32, D=128, bf16, QKV in pinned host, 16 GiB budget -> depth 2;
+    peak device bytes <= budget; sampled rows vs the oracle."""
+    B, H, N, D = 1, 32, 1_000_000, 128
+    budget = 16 << 30
+    q, k, v = host_qkv(B, H, N, D, 20260419, torch.bfloat16)
+    out, lse, info, st, peak = run_streamed(q, k, v, budget)
+    assert info.depth == 2 and peak <= budget
+    rng = np.random.default_rng(2)
+    for h in rng.choice(H, 2, replace=False):
+        rows = np.sort(rng.choice(N, 16, replace=False))
+        Oref, lref = O.dense_attention_rows(q[0, h].double().numpy(), k[0, h].double().numpy(),
+                                            v[0, h].double().numpy(), rows, block=65536)
+        o = out[0, h, rows].double().numpy()
+        assert np.abs(o - Oref).max() <= 2e-2
+        assert np.abs(lse[0, h, rows].double().numpy() - lref).max() <= 1e-3
