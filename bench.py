@@ -171,6 +171,7 @@ def main():
     import torch.distributed as dist
     import cqs_synth
     import paper_2604_20819_b200 as cqs
+    from paper_2604_20819_b200 import dist as cdist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -200,10 +201,6 @@ def main():
         base = ws.data_ptr()
         acc_o = ws[ao - base: ao - base + N * BH * D * 4].view(torch.float32).view(N, BH * D)
         acc_l = ws[al - base: al - base + N * BH * 4].view(torch.float32).view(N, BH)
-        spans = [cqs.cqs_shard_rows(N, world, r) for r in range(world)]
-        splits = [n for _, n in spans]
-        recv_o = torch.empty(world * my_rows, BH * D, dtype=torch.float32, device=dev)
-        recv_l = torch.empty(world * my_rows, BH, dtype=torch.float32, device=dev)
 
     flops = 4.0 * N * N * D * BH
 
@@ -212,12 +209,8 @@ def main():
         st = cqs.cqs_attention_forward(p, q, k, v, out, lse if world == 1 else None, 0.0, 0, ws,
                                        None, stream, stats=with_stats)
         if world > 1:                                     # a5: one exchange + R-way merge
-            dist.all_to_all_single(recv_o, acc_o, [my_rows] * world, splits)
-            dist.all_to_all_single(recv_l, acc_l, [my_rows] * world, splits)
-            po = [recv_o[r * my_rows:(r + 1) * my_rows] for r in range(world)]
-            pl = [recv_l[r * my_rows:(r + 1) * my_rows] for r in range(world)]
-            cqs.cqs_merge(my_rows, B, H, D, po, pl, out=out, out_row0=row0, n_total=N,
-                          lse_out=lse)
+            ro, rl, r0, nr = cdist.exchange_partials(acc_o, acc_l, N, world, rank)
+            cdist.merge_shard_gpu(ro, rl, world, nr, B, H, D, out, lse, r0, N, stream)
         return st
 
     for _ in range(args.warmup):

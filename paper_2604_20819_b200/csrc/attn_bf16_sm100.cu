@@ -91,7 +91,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // ---- work item: (query segment, 256-row pair) x (b,h) plane ----
-  const int item = blockIdx.x / tp.BH, bh = blockIdx.x % tp.BH;
+  // head-major rasterization: the ~148 CTAs in flight work on the same (b,h) plane and stream the
+  // same K/V tiles, so K/V come from L2 instead of being re-read from HBM by every CTA
+  const int bh = blockIdx.x / tp.n_items, item = blockIdx.x % tp.n_items;
   int oi = 0;
   while (item >= tp.item_end[oi]) ++oi;
   const int a = tp.order[oi];
@@ -252,10 +254,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           for (int c = 0; c < kBN; ++c)
             if (c >= valid) s[c] = -INFINITY;
         }
-        float mx = s[0];
+        // row max with 4 independent chains (breaks the dependent FMNMX latency chain)
+        float mx4[4] = {s[0], s[1], s[2], s[3]};
 #pragma unroll
-        for (int c = 1; c < kBN; ++c) mx = fmaxf(mx, s[c]);
-        mx *= scale_log2;
+        for (int c = 4; c < kBN; c += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) mx4[u] = fmaxf(mx4[u], s[c + u]);
+        }
+        float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale_log2;
         const float m_new = (j == 0 || mx > m + kRescaleThreshold) ? mx : m;
         const bool need = (j > 0) && (m_new != m);
         if (__any_sync(0xffffffffu, need)) {
@@ -276,7 +282,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           l *= f;
         }
         m = m_new;
-        float rs = 0.f;
+        float rs4[4] = {0.f, 0.f, 0.f, 0.f};   // 4 independent partial row sums
 #pragma unroll
         for (int c = 0; c < kBN / 32; ++c) {   // P (bf16 pairs) over S's first 64 columns
           uint32_t pk[16];
@@ -284,12 +290,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           for (int i = 0; i < 16; ++i) {
             const float p0 = ptx::ex2(fmaf(s[32 * c + 2 * i], scale_log2, -m));
             const float p1 = ptx::ex2(fmaf(s[32 * c + 2 * i + 1], scale_log2, -m));
-            rs += p0 + p1;
+            rs4[i & 3] += p0 + p1;
             pk[i] = ptx::pack_bf16(p0, p1);
           }
           ptx::tmem_st16(tS + c * 16, pk);
         }
-        l += rs;
+        l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();

@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(kF32Threads)
   float(*sV)[D] = reinterpret_cast<float(*)[D]>(f32_smem + kF32Rows * D + kF32Keys * (D + 1));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int item = blockIdx.x / tp.BH, bh = blockIdx.x % tp.BH;
+  const int bh = blockIdx.x / tp.n_items, item = blockIdx.x % tp.n_items;  // head-major
   int oi = 0;
   while (item >= tp.item_end[oi]) ++oi;
   const int a = tp.order[oi];

@@ -1,0 +1,52 @@
+"""Multi-GPU exchange for task-sharded CQS attention.
+
+Every rank runs `cqs_attention_forward` on the tasks its plan assigns to it (LPT on exact work, no
+communication during compute).  Each rank's fp32 partial accumulator ([N][B*H][D] + [N][B*H], see
+`cqs_partial_view`) is then exchanged ONCE: all-to-all of partial rows to the owner of each
+contiguous row shard (`cqs_shard_rows`), after which the owner LSE-merges the R partials of its rows
+(`cqs_merge` on the GPU).  torch.distributed is the transport (NCCL on GPUs, gloo in CPU tests):
+plumbing only — no arithmetic happens here.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import cqs_shard_rows
+
+
+def shard_spans(N: int, world: int):
+    """[(row0, rows)] per rank (the owner shards of the final merge)."""
+    return [cqs_shard_rows(N, world, r) for r in range(world)]
+
+
+def exchange_partials(acc_o: torch.Tensor, acc_l: torch.Tensor, N: int, world: int, rank: int,
+                      group=None):
+    """acc_o: [N, B*H*D] fp32 partial of this rank; acc_l: [N, B*H].  Returns (recv_o, recv_l,
+    row0, rows): the partials of this rank's shard from every rank, rank-major
+    ([world*rows, B*H*D] and [world*rows, B*H])."""
+    spans = shard_spans(N, world)
+    row0, rows = spans[rank]
+    in_splits = [n for _, n in spans]
+    out_splits = [rows] * world
+    recv_o = acc_o.new_empty((world * rows, acc_o.shape[1]))
+    recv_l = acc_l.new_empty((world * rows, acc_l.shape[1]))
+    dist.all_to_all_single(recv_o, acc_o.contiguous(), out_splits, in_splits, group=group)
+    dist.all_to_all_single(recv_l, acc_l.contiguous(), out_splits, in_splits, group=group)
+    return recv_o, recv_l, row0, rows
+
+
+def split_parts(recv_o: torch.Tensor, recv_l: torch.Tensor, world: int, rows: int):
+    """Per-rank views of the received partials, in rank order (fixed merge order)."""
+    po = [recv_o[r * rows:(r + 1) * rows] for r in range(world)]
+    pl = [recv_l[r * rows:(r + 1) * rows] for r in range(world)]
+    return po, pl
+
+
+def merge_shard_gpu(recv_o, recv_l, world, rows, B, H, D, out, lse, row0, N, stream=None):
+    """R-way LSE merge of the received partials into rows [row0, row0+rows) of out / lse
+    (cqs_merge kernel on the GPU)."""
+    from . import cqs_merge
+    po, pl = split_parts(recv_o, recv_l, world, rows)
+    cqs_merge(rows, B, H, D, po, pl, out=out, out_row0=row0, n_total=N, lse_out=lse,
+              stream=stream)

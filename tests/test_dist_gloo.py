@@ -1,0 +1,84 @@
+"""World-size-2 CPU (gloo) coverage of the multi-GPU path's host logic:
+the C++ planner's LPT task assignment, the row shards, and the all-to-all exchange layout.
+Each rank computes the partials of ITS tasks with the oracle (the GPU kernels need a device), the
+exchange runs through paper_2604_20819_b200.dist over gloo, and the owner merges its shard with the
+oracle's LSE merge; the union of shards must equal dense attention."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+I = (0, 1, 3)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, N, H, D, depth, outdir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import cqs_synth
+    import paper_2604_20819_b200 as cqs
+    from paper_2604_20819_b200 import dist as cdist
+    from oracle import cqs_oracle as O
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    q, k, v = (cqs_synth.numpy_tensor((1, H, N, D), 77, n) for n in ("q", "k", "v"))
+    plan = cqs.cqs_plan(N=N, B=1, H=H, D=D, depth=depth, in_dtype="f32", world=world, rank=rank)
+    info = plan.info()
+    # this rank's partial accumulator [N][H][D] + [N][H] (lse = -inf: nothing yet)
+    acc_o = np.zeros((N, H, D))
+    acc_l = np.full((N, H), -np.inf)
+    mine = 0
+    for t in range(info.n_tasks):
+        task = plan.task(t)
+        if task.rank != rank:
+            continue
+        mine += 1
+        e = O.build_subseq_entry(N, 7, I, tuple(task.quorum[i] for i in range(depth)))
+        Oi, li = O.task_partial(q, k, v, e)
+        idx = e.token_ids
+        mo, ml = O.lse_merge([(acc_o[idx], acc_l[idx]),
+                              (Oi[0].transpose(1, 0, 2), li[0].transpose(1, 0))])
+        acc_o[idx], acc_l[idx] = mo, ml
+    assert mine == info.my_tasks
+    ro, rl, row0, rows = cdist.exchange_partials(
+        torch.from_numpy(acc_o.reshape(N, H * D)), torch.from_numpy(acc_l), N, world, rank)
+    po, pl = cdist.split_parts(ro, rl, world, rows)
+    Om, lm = O.lse_merge([(p.numpy().reshape(rows, H, D), l_.numpy()) for p, l_ in zip(po, pl)])
+    np.save(os.path.join(outdir, "o%d.npy" % rank), Om)
+    np.save(os.path.join(outdir, "l%d.npy" % rank), lm)
+    np.save(os.path.join(outdir, "w%d.npy" % rank), np.array([info.my_work_pairs, row0, rows]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("N,depth", [(343, 3), (448, 1), (1030, 2)])
+def test_two_rank_exchange_reproduces_dense(N, depth, tmp_path):
+    import cqs_synth
+    from oracle import cqs_oracle as O
+    world, H, D = 2, 2, 32
+    mp.start_processes(_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path)),
+                       nprocs=world, start_method="fork")
+    q, k, v = (cqs_synth.numpy_tensor((1, H, N, D), 77, n) for n in ("q", "k", "v"))
+    Od, ld = O.dense_attention(q, k, v)
+    Od = Od[0].transpose(1, 0, 2)
+    ld = ld[0].transpose(1, 0)
+    tot_work = 0
+    for r in range(world):
+        w, row0, rows = np.load(tmp_path / ("w%d.npy" % r))
+        tot_work += w
+        Om = np.load(tmp_path / ("o%d.npy" % r))
+        lm = np.load(tmp_path / ("l%d.npy" % r))
+        assert np.abs(Om - Od[row0:row0 + rows]).max() < 1e-12
+        assert np.abs(lm - ld[row0:row0 + rows]).max() < 1e-12
+    assert tot_work == N * N
