@@ -1,0 +1,7 @@
+nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw --format=csv -lms 100 > gpurun_out/r01_mufu_clocks.csv &
+SMI=$!
+./tools/mufu_bench
+kill $SMI
+timeout 900 python -m pytest tests -x -q -m "gpu and not slow" 2>&1 | tail -4
+timeout 300 python bench.py --steps 3 --warmup 2 --no-cpu --no-e2e 2>&1 | tail -1
+timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"merge|fill" -c 4 --csv --log-file gpurun_out/r01c_merge.csv python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e > /dev/null 2>&1; echo ncu rc=$?

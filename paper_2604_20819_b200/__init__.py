@@ -15,7 +15,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcqs.so")
+LIB_PATH = os.environ.get("CQS_LIB") or os.path.join(_HERE, "libcqs.so")  # CQS_LIB: debug variants
 
 CQS_OK, CQS_E_VERIFY, CQS_E_INFEASIBLE, CQS_E_INVALID, CQS_E_CUDA, CQS_E_NCCL, CQS_E_OOM, \
     CQS_E_UNSUPPORTED = range(8)

@@ -22,14 +22,21 @@
 #include <cuda_runtime.h>
 
 #include "ptx.cuh"
+#include "attn_common.cuh"
 #include "task_params.cuh"
 
 namespace cqs {
 
-constexpr int kBM = 128;   // query rows per tile (TMEM lanes)
-constexpr int kBN = 128;   // keys per KV tile
 constexpr int kAttnThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
+// column pairs (i mod 8) whose exp2 runs on the FMA pipe instead of MUFU
+// (measured on B200, C2 shape: at D=128 MUFU-only is fastest under the power cap — 958 vs 910
+// TFLOP/s with 3/8 emulated; at D=64 the MUFU bound dominates and 3/8 emulation gains ~1%)
+#ifdef CQS_DBG_POLY_MASK
+template <int D> constexpr uint32_t kPolyMask = CQS_DBG_POLY_MASK;
+#else
+template <int D> constexpr uint32_t kPolyMask = D == 64 ? 0x25 : 0x0;
+#endif
 
 template <int D>
 struct AttnCfg {
@@ -39,31 +46,6 @@ struct AttnCfg {
   static constexpr int kStages = D == 128 ? 4 : 8;
   static constexpr int kSmemBytes = 2 * kQBytes + kStages * kKVBytes + 1024 + 512;
   static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
-};
-
-// Iterates the key tiles of the kept key segments of one query segment (ascending segment id).
-struct KvCursor {
-  uint32_t mask;
-  int seg, kt, ntile;
-  const TaskParams* tp;
-  __device__ __forceinline__ void set_seg() {
-    seg = mask ? __ffs(mask) - 1 : 0;
-    kt = 0;
-    ntile = mask ? (tp->seg_len[seg] + kBN - 1) / kBN : 0;
-  }
-  __device__ __forceinline__ void init(const TaskParams* p, uint32_t m) {
-    tp = p;
-    mask = m;
-    set_seg();
-  }
-  __device__ __forceinline__ int row() const { return tp->seg_src[seg] + kt * kBN; }
-  __device__ __forceinline__ int valid() const { return min(kBN, tp->seg_len[seg] - kt * kBN); }
-  __device__ __forceinline__ void next() {
-    if (++kt == ntile) {
-      mask &= mask - 1;
-      set_seg();
-    }
-  }
 };
 
 template <int D>
@@ -145,6 +127,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                            q_row + t * kBM, hi, bi);
       int it = 0;
       auto load = [&](const CUtensorMap* map, int row) {
+#ifdef CQS_DBG_NO_TMA_REFILL
+        if (it >= C::kStages) return;
+#endif
         const int s = it % C::kStages;
         const uint32_t ph = (it / C::kStages) & 1;
         ptx::mbar_wait(&kv_empty[s], ph ^ 1);
@@ -207,15 +192,23 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         int sKn = -1;
         if (j + 1 < n_kv) {
           sKn = it % C::kStages;
+#ifdef CQS_DBG_NO_TMA_REFILL
+          if (it < C::kStages)
+#endif
           ptx::mbar_wait(&kv_full[sKn], (it / C::kStages) & 1);
           ++it;
         }
         const int sV = it % C::kStages;
+#ifdef CQS_DBG_NO_TMA_REFILL
+        if (it < C::kStages)
+#endif
         ptx::mbar_wait(&kv_full[sV], (it / C::kStages) & 1);
         ++it;
         ptx::tc_fence_after();
         for (int t = 0; t < (two ? 2 : 1); ++t) {
+#ifndef CQS_DBG_NO_PWAIT
           ptx::mbar_wait(&p_full[t], j & 1);
+#endif
           ptx::tc_fence_after();
           issue_PV(t, sV, j > 0);
           if (sKn >= 0) issue_S(t, sKn);
@@ -223,6 +216,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         ptx::mma_commit(&kv_empty[sV]);
         if (sKn >= 0) ptx::mma_commit(&kv_empty[sKn]);
       }
+      // drain: q_full's second phase completes when every MMA of this CTA has retired
+      ptx::mma_commit(q_full);
+      ptx::mbar_wait(q_full, 1);
     }
   }
   } else {
@@ -243,6 +239,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         cur.next();
         ptx::mbar_wait(&s_full[t], j & 1);
         ptx::tc_fence_after();
+#ifdef CQS_DBG_NO_PWAIT   // timing experiment only: softmax warps do nothing
+        break;
+#endif
+#ifdef CQS_DBG_SKIP_SOFTMAX   // timing experiment only: tensor/TMA pipeline without softmax work
+        if (j == 0) m = 0.f, l = 1.f;
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+        continue;
+#endif
         uint32_t sr[kBN];
 #pragma unroll
         for (int c = 0; c < kBN / 32; ++c)
@@ -282,20 +288,48 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           l *= f;
         }
         m = m_new;
-        float rs4[4] = {0.f, 0.f, 0.f, 0.f};   // 4 independent partial row sums
+        // p = 2^(s*scale_log2 - m): packed FFMA2 for the argument, then MUFU.EX2 for most column
+        // pairs and the FMA-pipe polynomial for the pairs selected by kPolyMask (load balance
+        // between the 16/clk/SM MUFU and the issue slots)
+        const uint64_t sc2 = ptx::f2(scale_log2, scale_log2), nm2 = ptx::f2(-m, -m);
+#pragma unroll
+        for (int i = 0; i < kBN / 2; ++i) {
+          float x0, x1;
+          ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
+#ifdef CQS_DBG_SKIP_EXP
+          if (true) {
+          } else
+#endif
+          if ((kPolyMask<D> >> (i & 7)) & 1) {
+            ptx::exp2_poly_pair(x0, x1);
+          } else {
+            x0 = ptx::ex2(x0);
+            x1 = ptx::ex2(x1);
+          }
+          s[2 * i] = x0;
+          s[2 * i + 1] = x1;
+        }
+        if (valid < kBN) {
+#pragma unroll
+          for (int c = 0; c < kBN; ++c)
+            if (c >= valid) s[c] = 0.f;
+        }
+        uint64_t rs2[4] = {0, 0, 0, 0};   // 4 independent packed partial row sums
+#pragma unroll
+        for (int i = 0; i < kBN / 2; ++i) rs2[i & 3] = ptx::fadd2(rs2[i & 3], ptx::f2(s[2 * i], s[2 * i + 1]));
+        {
+          const uint64_t r = ptx::fadd2(ptx::fadd2(rs2[0], rs2[1]), ptx::fadd2(rs2[2], rs2[3]));
+          float a0, a1;
+          ptx::f2_split(r, a0, a1);
+          l += a0 + a1;
+        }
 #pragma unroll
         for (int c = 0; c < kBN / 32; ++c) {   // P (bf16 pairs) over S's first 64 columns
           uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float p0 = ptx::ex2(fmaf(s[32 * c + 2 * i], scale_log2, -m));
-            const float p1 = ptx::ex2(fmaf(s[32 * c + 2 * i + 1], scale_log2, -m));
-            rs4[i & 3] += p0 + p1;
-            pk[i] = ptx::pack_bf16(p0, p1);
-          }
+          for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]);
           ptx::tmem_st16(tS + c * 16, pk);
         }
-        l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
@@ -353,9 +387,27 @@ static cudaError_t launch_bf16_impl(const CUtensorMap* maps, const TaskParams& t
   return cudaGetLastError();
 }
 
+cudaError_t launch_attn_bf16_pair(const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
+                                  float* acc_lse, float scale, cudaStream_t stream);
+
+// D = 128 runs on CTA pairs (cta_group::2, 512 query rows per item; K maps with 64-row boxes);
+// D = 64 on single CTAs (256 rows per item).  Callers size work items with attn_rows_per_item
+// and build maps with attn_kv_box_rows.
+#ifndef CQS_ONE_CTA_D128
+int attn_rows_per_item(int D) { return D == 128 ? 512 : 256; }
+int attn_k_box_rows(int D) { return D == 128 ? 64 : 128; }
+#else
+int attn_rows_per_item(int) { return 256; }
+int attn_k_box_rows(int) { return 128; }
+#endif
+
 cudaError_t launch_attn_bf16(int D, const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
                              float* acc_lse, float scale, cudaStream_t stream) {
+#ifndef CQS_ONE_CTA_D128
+  if (D == 128) return launch_attn_bf16_pair(maps, tp, acc_o, acc_lse, scale, stream);
+#else
   if (D == 128) return launch_bf16_impl<128>(maps, tp, acc_o, acc_lse, scale, stream);
+#endif
   if (D == 64) return launch_bf16_impl<64>(maps, tp, acc_o, acc_lse, scale, stream);
   return cudaErrorInvalidValue;
 }

@@ -1,0 +1,337 @@
+// Per-task CQS attention kernel for D = 128 on a CTA PAIR (tcgen05 cta_group::2, M = 256).
+//
+// Same math and contract as attn_bf16_sm100.cu (Eq. 2 partial in FA form, P:43 / P:240, merged
+// into the fp32 accumulator in the epilogue, Eq. 3), but each MMA spans two SMs:
+//   S_t = Q_t K^T : M = 256 query rows (128 per CTA, A from each CTA's smem), N = 128 keys split
+//                   64 / 64 between the CTAs' smem (B operand), fp32 result: each CTA's TMEM
+//                   holds its 128 rows x 128 keys
+//   O_t += P_t V  : A = P from each CTA's TMEM, B = V split by head-dim columns 64 / 64
+// so every SM stages only HALF of each K and V tile (TMA and shared-memory operand traffic per SM
+// halve vs the 1-CTA kernel: measured 1-CTA pure-MMA ceiling was 76% of the tensor peak).
+//
+// Cluster (2,1,1) = one work item = 512 query rows of one query segment of one (b,h) plane:
+// CTA r, tile t owns rows base + 256 t + 128 r.  Warp roles per CTA as in the 1-CTA kernel
+// (TMA producer, MMA issuer [leader CTA only], TMEM allocator, 2 x 4 softmax warps).  Barrier
+// protocol: kv_full / q_full / p_full live in the LEADER (both CTAs' TMA bytes and both CTAs'
+// softmax arrivals land there); s_full / o_bar / kv_empty exist in both CTAs and are signalled by
+// the leader's multicast tcgen05.commit.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "attn_common.cuh"
+#include "ptx.cuh"
+
+namespace cqs {
+
+namespace pair {
+constexpr int D = 128;
+constexpr int kThreads = 384;
+constexpr int kQBytes = kBM * D * 2;           // one 128-row Q tile (two 64-col boxes)
+constexpr int kKHalfRows = kBN / 2;            // keys per CTA in a K tile
+constexpr int kStageBytes = 16384;             // K half (2 boxes of 64 rows) or V half (1 box)
+constexpr int kStages = 8;
+constexpr int kSmemBytes = 2 * kQBytes + kStages * kStageBytes + 1024 + 512;
+constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 384;
+constexpr float kRescaleThreshold = 8.0f;
+}  // namespace pair
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
+    attn_bf16_sm100_2cta_kernel(const __grid_constant__ CUtensorMap tmQ,
+                                const __grid_constant__ CUtensorMap tmK,   // box 64 x 64
+                                const __grid_constant__ CUtensorMap tmV,   // box 64 x 128
+                                const __grid_constant__ TaskParams tp, float* __restrict__ acc_o,
+                                float* __restrict__ acc_lse, float scale_log2) {
+  using namespace pair;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;                                  // [2 tiles][2 boxes][128][128 B]
+  uint8_t* sKV = smem + 2 * kQBytes;                   // [kStages][16 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + kStages * kStageBytes);
+  uint64_t* q_full = bars;                             // leader: Q bytes of both CTAs; + drain
+  uint64_t* kv_full = bars + 1;                        // leader: K/V half bytes of both CTAs
+  uint64_t* kv_empty = kv_full + kStages;              // both: stage free (multicast commit)
+  uint64_t* s_full = kv_empty + kStages;               // both: S_t ready (multicast commit)
+  uint64_t* p_full = s_full + 2;                       // leader: 8 softmax warps of the pair
+  uint64_t* o_bar = p_full + 2;                        // both: PV_t retired (multicast commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+
+  // ---- work item: cluster id -> (b,h) plane (head-major) x (query segment, 512-row block) ----
+  const int cid = blockIdx.x >> 1;
+  const int bh = cid / tp.n_items, item = cid % tp.n_items;
+  int oi = 0;
+  while (item >= tp.item_end[oi]) ++oi;
+  const int a = tp.order[oi];
+  const int q_off = (item - (oi ? tp.item_end[oi - 1] : 0)) * (4 * kBM);
+  const int len_a = tp.seg_len[a];
+  const bool two = len_a - q_off > 2 * kBM;            // tile 1 has rows in either CTA
+  const int bi = bh / tp.H, hi = bh % tp.H;
+  const uint32_t kmask = tp.kept[a];
+  int n_kv = 0;
+  for (uint32_t m = kmask; m; m &= m - 1) n_kv += (tp.seg_len[__ffs(m) - 1] + kBN - 1) / kBN;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 1);
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&kv_full[s], 1);
+      ptx::mbar_init(&kv_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(&s_full[t], 1);
+      ptx::mbar_init(&p_full[t], 8);
+      ptx::mbar_init(&o_bar[t], 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_2sm(tmem_slot, 512);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();      // barriers of both CTAs initialised, TMEM allocated in both
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
+    if (warp == 0 && lane == 0) {
+      // ================= TMA producer (both CTAs) =================
+      ptx::tma_prefetch_desc(&tmQ);
+      ptx::tma_prefetch_desc(&tmK);
+      ptx::tma_prefetch_desc(&tmV);
+      const int q_row = tp.seg_src[a] + q_off + int(rank) * kBM;
+      const int ntile = two ? 2 : 1;
+      if (leader) ptx::mbar_arrive_expect_tx(q_full, 2 * ntile * kQBytes);
+      for (int t = 0; t < ntile; ++t)
+        for (int bx = 0; bx < 2; ++bx)
+          ptx::tma_load_4d_2sm(sQ + t * kQBytes + bx * kBM * 128, &tmQ, q_full, bx * 64,
+                               q_row + t * 2 * kBM, hi, bi);
+      int it = 0;
+      auto stage_wait = [&](int s) {
+        ptx::mbar_wait(&kv_empty[s], ((it / kStages) & 1) ^ 1);
+        if (leader) ptx::mbar_arrive_expect_tx(&kv_full[s], 2 * kStageBytes);
+      };
+      KvCursor ck, cv;
+      ck.init(&tp, kmask);
+      cv.init(&tp, kmask);
+      auto load_k = [&]() {   // keys [64 rank, 64 rank + 64) of the tile, both 64-col boxes
+        const int s = it % kStages;
+        stage_wait(s);
+        for (int bx = 0; bx < 2; ++bx)
+          ptx::tma_load_4d_2sm(sKV + s * kStageBytes + bx * kKHalfRows * 128, &tmK, &kv_full[s],
+                               bx * 64, ck.row() + int(rank) * kKHalfRows, hi, bi);
+        ck.next();
+        ++it;
+      };
+      auto load_v = [&]() {   // head-dim columns [64 rank, 64 rank + 64) of all 128 keys
+        const int s = it % kStages;
+        stage_wait(s);
+        ptx::tma_load_4d_2sm(sKV + s * kStageBytes, &tmV, &kv_full[s], int(rank) * 64, cv.row(),
+                             hi, bi);
+        cv.next();
+        ++it;
+      };
+      load_k();
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) load_k();
+        load_v();
+      }
+    } else if (warp == 1 && lane == 0 && leader) {
+      // ================= MMA issuer (leader CTA, one thread) =================
+      constexpr uint32_t idesc_qk = ptx::idesc_bf16(2 * kBM, kBN, 0, 0);   // M=256, N=128
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16(2 * kBM, D, 0, 1);     // M=256, N=128
+      const uint32_t sq = ptx::smem_u32(sQ), skv = ptx::smem_u32(sKV);
+      const uint32_t colS[2] = {kColS0, kColS1}, colO[2] = {kColO0, kColO1};
+      auto issue_S = [&](int t, int s) {
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t kb = (ks & 3) * 32;
+          const uint64_t ad =
+              ptx::smem_desc_sw128(sq + t * kQBytes + (ks >> 2) * (kBM * 128) + kb, 16, 1024);
+          const uint64_t bd =
+              ptx::smem_desc_sw128(skv + s * kStageBytes + (ks >> 2) * (kKHalfRows * 128) + kb,
+                                   16, 1024);
+          ptx::mma_ss_2sm(tmem + colS[t], ad, bd, idesc_qk, ks > 0);
+        }
+        ptx::mma_commit_2sm(&s_full[t]);
+      };
+      auto issue_PV = [&](int t, int s, bool acc) {
+#pragma unroll
+        for (int ks = 0; ks < kBN / 16; ++ks) {
+          const uint64_t bd = ptx::smem_desc_sw128(skv + s * kStageBytes + ks * 16 * 128,
+                                                   kBN * 128, 1024);
+          ptx::mma_ts_2sm(tmem + colO[t], tmem + colS[t] + ks * 8, bd, idesc_pv,
+                          (acc || ks > 0));
+        }
+        ptx::mma_commit_2sm(&o_bar[t]);
+      };
+      int it = 0;
+      ptx::mbar_wait(q_full, 0);
+      const int sK0 = it % kStages;
+      ptx::mbar_wait(&kv_full[sK0], (it / kStages) & 1);
+      ++it;
+      ptx::tc_fence_after();
+      issue_S(0, sK0);
+      if (two) issue_S(1, sK0);
+      ptx::mma_commit_2sm(&kv_empty[sK0]);
+      for (int j = 0; j < n_kv; ++j) {
+        int sKn = -1;
+        if (j + 1 < n_kv) {
+          sKn = it % kStages;
+          ptx::mbar_wait(&kv_full[sKn], (it / kStages) & 1);
+          ++it;
+        }
+        const int sV = it % kStages;
+        ptx::mbar_wait(&kv_full[sV], (it / kStages) & 1);
+        ++it;
+        ptx::tc_fence_after();
+        for (int t = 0; t < (two ? 2 : 1); ++t) {
+          ptx::mbar_wait(&p_full[t], j & 1);
+          ptx::tc_fence_after();
+          issue_PV(t, sV, j > 0);
+          if (sKn >= 0) issue_S(t, sKn);
+        }
+        ptx::mma_commit_2sm(&kv_empty[sV]);
+        if (sKn >= 0) ptx::mma_commit_2sm(&kv_empty[sKn]);
+      }
+      ptx::mma_commit_2sm(q_full);   // drain: all MMAs of the pair retired
+      ptx::mbar_wait(q_full, 1);
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
+    // ================= softmax / correction / epilogue (both CTAs) =================
+    const int t = (warp - 4) >> 2;
+    if (t == 0 || two) {
+      const int sub = warp & 3;
+      const int r = sub * 32 + lane;
+      const uint32_t lane_base = uint32_t(sub * 32) << 16;
+      const uint32_t tS = tmem + lane_base + (t ? kColS1 : kColS0);
+      const uint32_t tO = tmem + lane_base + (t ? kColO1 : kColO0);
+      float m = -INFINITY, l = 0.f;
+      KvCursor cur;
+      cur.init(&tp, kmask);
+      for (int j = 0; j < n_kv; ++j) {
+        const int valid = cur.valid();
+        cur.next();
+        ptx::mbar_wait(&s_full[t], j & 1);
+        ptx::tc_fence_after();
+        uint32_t sr[kBN];
+#pragma unroll
+        for (int c = 0; c < kBN / 32; ++c)
+          ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+        ptx::tmem_ld_wait();
+        float* s = reinterpret_cast<float*>(sr);
+        if (valid < kBN) {
+#pragma unroll
+          for (int c = 0; c < kBN; ++c)
+            if (c >= valid) s[c] = -INFINITY;
+        }
+        float mx4[4] = {s[0], s[1], s[2], s[3]};
+#pragma unroll
+        for (int c = 4; c < kBN; c += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) mx4[u] = fmaxf(mx4[u], s[c + u]);
+        }
+        const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale_log2;
+        const float m_new = (j == 0 || mx > m + kRescaleThreshold) ? mx : m;
+        const bool need = (j > 0) && (m_new != m);
+        if (__any_sync(0xffffffffu, need)) {
+          ptx::mbar_wait(&o_bar[t], (j - 1) & 1);
+          ptx::tc_fence_after();
+          const float f = need ? ptx::ex2(m - m_new) : 1.f;
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t ov[32];
+            ptx::tmem_ld32(tO + c * 32, ov);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * f);
+            ptx::tmem_st32(tO + c * 32, ov);
+          }
+          ptx::tmem_st_wait();
+          l *= f;
+        }
+        m = m_new;
+        const uint64_t sc2 = ptx::f2(scale_log2, scale_log2), nm2 = ptx::f2(-m, -m);
+#pragma unroll
+        for (int i = 0; i < kBN / 2; ++i) {
+          float x0, x1;
+          ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
+          s[2 * i] = ptx::ex2(x0);
+          s[2 * i + 1] = ptx::ex2(x1);
+        }
+        uint64_t rs2[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < kBN / 2; ++i)
+          rs2[i & 3] = ptx::fadd2(rs2[i & 3], ptx::f2(s[2 * i], s[2 * i + 1]));
+        {
+          const uint64_t rr = ptx::fadd2(ptx::fadd2(rs2[0], rs2[1]), ptx::fadd2(rs2[2], rs2[3]));
+          float a0, a1;
+          ptx::f2_split(rr, a0, a1);
+          l += a0 + a1;
+        }
+#pragma unroll
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]);
+          ptx::tmem_st16(tS + c * 16, pk);
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_leader(&p_full[t]);
+      }
+      // ---- epilogue ----
+      ptx::mbar_wait(&o_bar[t], (n_kv - 1) & 1);
+      ptx::tc_fence_after();
+      const int row_in_seg = q_off + t * 2 * kBM + int(rank) * kBM + r;
+      const bool live = row_in_seg < len_a;
+      const float inv_l = 1.f / l;
+      const float lse = (m + __log2f(l)) * 0.69314718055994531f;
+      const int64_t idx = int64_t(tp.seg_dst[a] + row_in_seg) * tp.BH + bh;
+      MergeW w{};
+      if (live) w = merge_weights(acc_lse[idx], lse);
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t ov[32];
+        ptx::tmem_ld32(tO + c * 32, ov);
+        ptx::tmem_ld_wait();
+        if (live) {
+          float o[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(ov[i]) * inv_l;
+          merge_chunk<32>(acc_o + idx * D + c * 32, o, w);
+        }
+      }
+      if (live) acc_lse[idx] = w.lse;
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();      // both CTAs done with TMEM / peer barriers before teardown
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_2sm(tmem, 512);
+  }
+}
+
+cudaError_t launch_attn_bf16_pair(const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
+                                  float* acc_lse, float scale, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bf16_sm100_2cta_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         pair::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int64_t grid = 2 * int64_t(tp.n_items) * tp.BH;
+  if (grid <= 0) return cudaSuccess;
+  attn_bf16_sm100_2cta_kernel<<<dim3(unsigned(grid)), pair::kThreads, pair::kSmemBytes, stream>>>(
+      maps[0], maps[1], maps[2], tp, acc_o, acc_lse, scale * 1.4426950408889634f);
+  return cudaGetLastError();
+}
+
+}  // namespace cqs

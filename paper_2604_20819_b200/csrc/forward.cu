@@ -27,6 +27,8 @@ cudaError_t launch_attn_f32(int D, const TaskParams& tp, const float* q, const f
                             const float* v, const int64_t* strides, float* acc_o, float* acc_lse,
                             float scale, cudaStream_t stream);
 cudaError_t launch_fill(float* p, int64_t n, float val, cudaStream_t st);
+int attn_rows_per_item(int D);
+int attn_k_box_rows(int D);
 cudaError_t launch_merge(int64_t rows, int B, int H, int D, int n_parts, const float* const* po,
                          const float* const* pl, float* acc_o, float* acc_lse, bool acc_write,
                          void* out, cqs_dtype out_dtype, const int64_t* out_strides,
@@ -178,11 +180,12 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
     const void* bases[3] = {q, k, v};
     for (int i = 0; i < 3; ++i) {
       cqs_status s = make_tmap_bf16(&maps[i], bases[i], d.B, d.H, d.N, d.D, qkv_strides[0],
-                                    qkv_strides[1], qkv_strides[2], 128);
+                                    qkv_strides[1], qkv_strides[2],
+                                    i == 1 ? attn_k_box_rows(d.D) : 128);
       if (s != CQS_OK) return s;
     }
   }
-  const int rows_per_item = d.in_dtype == CQS_BF16 ? 256 : 32;
+  const int rows_per_item = d.in_dtype == CQS_BF16 ? attn_rows_per_item(d.D) : 32;
   TaskParams tp;
   int64_t run = 0;
   for (int64_t ti : p->my_order) {

@@ -1,6 +1,6 @@
 // LSE merge / finalize kernels (Eq. 3 in LSE form, PAPER.md P:48-52 with Den_j = exp(lse_j),
-// Num_j = O_j Den_j).  HBM-bound: one warp per (row, plane), 16-byte vector loads of the
-// D-contiguous fp32 rows, coalesced across the warp; bf16/fp32 output cast fused.
+// Num_j = O_j Den_j).  HBM-bound: flat 16-byte vector loads of the D-contiguous fp32 rows,
+// coalesced across the warp, several loads in flight per thread; bf16/fp32 output cast fused.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -33,71 +33,131 @@ __device__ __forceinline__ void store4(__nv_bfloat16* dst, float4 v) {
   *reinterpret_cast<uint2*>(dst) = u;
 }
 
-// rows x planes, one warp each.  Parts are [rows][BH][D]; acc (optional) likewise.
+// One warp per (row, plane) unit per step, kUnits units per warp iteration so that every lane has
+// kUnits x (parts + 1) independent 16-byte loads in flight; the LSE weights of a unit are computed
+// redundantly by the 32 lanes (per unit, not per element).
+constexpr int kUnits = 4;
+
+__device__ __forceinline__ void unit_weights(const MergeParts& parts, const float* acc_lse,
+                                             int64_t unit, float (&w)[kMaxMergeParts + 1],
+                                             float& lse) {
+  const float la = acc_lse ? acc_lse[unit] : -INFINITY;
+  float mx = la;
+  for (int j = 0; j < parts.n; ++j) mx = fmaxf(mx, parts.l[j][unit]);
+  if (mx == -INFINITY) {
+#pragma unroll
+    for (int j = 0; j <= kMaxMergeParts; ++j) w[j] = 0.f;
+    lse = -INFINITY;
+    return;
+  }
+  float s = 0.f;
+  w[kMaxMergeParts] = la != -INFINITY ? expf(la - mx) : 0.f;
+  s += w[kMaxMergeParts];
+#pragma unroll
+  for (int j = 0; j < kMaxMergeParts; ++j) {
+    float x = 0.f;
+    if (j < parts.n) {
+      const float lj = parts.l[j][unit];
+      x = lj != -INFINITY ? expf(lj - mx) : 0.f;
+    }
+    w[j] = x;
+    s += x;
+  }
+  const float inv = 1.f / s;
+#pragma unroll
+  for (int j = 0; j <= kMaxMergeParts; ++j) w[j] *= inv;
+  lse = mx + logf(s);
+}
+
 template <typename OutT>
 __global__ void __launch_bounds__(256)
     merge_kernel(int64_t rows, int BH, int H, int D, MergeParts parts, float* __restrict__ acc_o,
                  float* __restrict__ acc_lse, bool acc_write, OutT* __restrict__ out, int64_t sB,
                  int64_t sH, int64_t sN, int64_t out_row0, int64_t n_total,
                  float* __restrict__ lse_out) {
-  const int64_t wid = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (wid >= rows * BH) return;
-  const int64_t r = wid / BH;
-  const int p = int(wid % BH);
-  const int64_t row_off = wid * D;
-  // weights
-  float mx = -INFINITY;
-  const float la = acc_lse ? acc_lse[wid] : -INFINITY;
-  mx = fmaxf(mx, la);
-  for (int j = 0; j < parts.n; ++j) mx = fmaxf(mx, parts.l[j][wid]);
-  float lse, wa = 0.f;
-  float w[kMaxMergeParts];
-  if (mx == -INFINITY) {
-    lse = -INFINITY;
-    for (int j = 0; j < kMaxMergeParts; ++j) w[j] = 0.f;
-  } else {
-    float s = 0.f;
-    if (la != -INFINITY) {
-      wa = expf(la - mx);
-      s += wa;
-    }
+  const int64_t nunits = rows * BH;
+  const int64_t warp0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int D4 = D >> 2;
+  for (int64_t u0 = warp0 * kUnits; u0 < nunits; u0 += nwarps * kUnits) {
+    for (int d4 = lane; d4 < D4; d4 += 32) {
+      float4 v[kUnits];
+      float lse[kUnits];
 #pragma unroll
-    for (int j = 0; j < kMaxMergeParts; ++j) {
-      w[j] = 0.f;
-      if (j < parts.n) {
-        const float lj = parts.l[j][wid];
-        if (lj != -INFINITY) w[j] = expf(lj - mx);
-        s += w[j];
+      for (int u = 0; u < kUnits; ++u) {
+        const int64_t unit = u0 + u;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (unit >= nunits) continue;
+        float w[kMaxMergeParts + 1];
+        unit_weights(parts, acc_lse, unit, w, lse[u]);
+        const int64_t f = unit * D4 + d4;
+        if (w[kMaxMergeParts] != 0.f) {
+          const float4 x = reinterpret_cast<const float4*>(acc_o)[f];
+          const float a = w[kMaxMergeParts];
+          v[u] = make_float4(a * x.x, a * x.y, a * x.z, a * x.w);
+        }
+        for (int j = 0; j < parts.n; ++j) {
+          if (w[j] == 0.f) continue;
+          const float4 x = reinterpret_cast<const float4*>(parts.o[j])[f];
+          v[u].x = fmaf(w[j], x.x, v[u].x);
+          v[u].y = fmaf(w[j], x.y, v[u].y);
+          v[u].z = fmaf(w[j], x.z, v[u].z);
+          v[u].w = fmaf(w[j], x.w, v[u].w);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnits; ++u) {
+        const int64_t unit = u0 + u;
+        if (unit >= nunits) continue;
+        if (acc_write) reinterpret_cast<float4*>(acc_o)[unit * D4 + d4] = v[u];
+        const int64_t r = unit / BH;
+        const int p = int(unit - r * BH);
+        if (out)
+          store4(out + int64_t(p / H) * sB + int64_t(p % H) * sH + (out_row0 + r) * sN + 4 * d4, v[u]);
+        if (d4 == 0) {
+          if (acc_write) acc_lse[unit] = lse[u];
+          if (lse_out) lse_out[int64_t(p) * n_total + out_row0 + r] = lse[u];
+        }
       }
     }
-    const float inv = 1.f / s;
-    wa *= inv;
+  }
+}
+
+// Finalize (no parts): O = acc_o (0 where acc_lse = -inf), lse = acc_lse; pure streaming copy+cast.
+constexpr int kFinVec = 4;
+template <typename OutT>
+__global__ void __launch_bounds__(256)
+    finalize_kernel(int64_t rows, int BH, int H, int D, const float* __restrict__ acc_o,
+                    const float* __restrict__ acc_lse, OutT* __restrict__ out, int64_t sB,
+                    int64_t sH, int64_t sN, int64_t out_row0, int64_t n_total,
+                    float* __restrict__ lse_out) {
+  const int D4 = D >> 2;
+  const int64_t n4 = rows * BH * D4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; b < n4; b += stride * kFinVec) {
+    float4 v[kFinVec];
+    float l[kFinVec];
 #pragma unroll
-    for (int j = 0; j < kMaxMergeParts; ++j) w[j] *= inv;
-    lse = mx + logf(s);
-  }
-  OutT* orow = out ? out + int64_t(p / H) * sB + int64_t(p % H) * sH + (out_row0 + r) * sN : nullptr;
-  for (int d = lane * 4; d < D; d += 128) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (wa != 0.f) {
-      const float4 a = *reinterpret_cast<const float4*>(acc_o + row_off + d);
-      acc.x = wa * a.x, acc.y = wa * a.y, acc.z = wa * a.z, acc.w = wa * a.w;
+    for (int u = 0; u < kFinVec; ++u) {
+      const int64_t f = b + u * stride;
+      if (f < n4) {
+        v[u] = reinterpret_cast<const float4*>(acc_o)[f];
+        l[u] = acc_lse[f / D4];
+      }
     }
-    for (int j = 0; j < parts.n; ++j) {
-      if (w[j] == 0.f) continue;
-      const float4 b = *reinterpret_cast<const float4*>(parts.o[j] + row_off + d);
-      acc.x = fmaf(w[j], b.x, acc.x);
-      acc.y = fmaf(w[j], b.y, acc.y);
-      acc.z = fmaf(w[j], b.z, acc.z);
-      acc.w = fmaf(w[j], b.w, acc.w);
+#pragma unroll
+    for (int u = 0; u < kFinVec; ++u) {
+      const int64_t f = b + u * stride;
+      if (f >= n4) continue;
+      const int64_t unit = f / D4;
+      const int d = int(f - unit * D4) * 4;
+      if (l[u] == -INFINITY) v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int64_t r = unit / BH;
+      const int p = int(unit - r * BH);
+      store4(out + int64_t(p / H) * sB + int64_t(p % H) * sH + (out_row0 + r) * sN + d, v[u]);
+      if (d == 0 && lse_out) lse_out[int64_t(p) * n_total + out_row0 + r] = l[u];
     }
-    if (acc_write) store4(acc_o + row_off + d, acc);
-    if (orow) store4(orow + d, acc);
-  }
-  if (lane == 0) {
-    if (acc_write) acc_lse[wid] = lse;
-    if (lse_out) lse_out[int64_t(p) * n_total + out_row0 + r] = lse;
   }
 }
 
@@ -119,12 +179,26 @@ cudaError_t launch_merge(int64_t rows, int B, int H, int D, int n_parts, const f
     mp.l[j] = pl[j];
   }
   const int BH = B * H;
-  const int64_t warps = rows * BH;
-  if (warps <= 0) return cudaSuccess;
-  const int64_t blocks = (warps * 32 + 255) / 256;
+  const int64_t nunits = rows * BH;
+  if (nunits <= 0) return cudaSuccess;
   const int64_t sB = out ? out_strides[0] : 0, sH = out ? out_strides[1] : 0,
                 sN = out ? out_strides[2] : 0;
-  if (!out || out_dtype == CQS_F32)
+  const bool bf = out && out_dtype == CQS_BF16;
+  if (n_parts == 0 && acc_o && !acc_write && out) {
+    const int64_t n4 = nunits * (D / 4);
+    const int64_t blocks = std::min<int64_t>((n4 + 256 * kFinVec - 1) / (256 * kFinVec), 148 * 32);
+    if (bf)
+      finalize_kernel<__nv_bfloat16><<<unsigned(blocks), 256, 0, st>>>(
+          rows, BH, H, D, acc_o, acc_lse, static_cast<__nv_bfloat16*>(out), sB, sH, sN, out_row0,
+          n_total, lse_out);
+    else
+      finalize_kernel<float><<<unsigned(blocks), 256, 0, st>>>(
+          rows, BH, H, D, acc_o, acc_lse, static_cast<float*>(out), sB, sH, sN, out_row0, n_total,
+          lse_out);
+    return cudaGetLastError();
+  }
+  const int64_t blocks = std::min<int64_t>((nunits + 8 * kUnits - 1) / (8 * kUnits), 148 * 32);
+  if (!bf)
     merge_kernel<float><<<unsigned(blocks), 256, 0, st>>>(
         rows, BH, H, D, mp, acc_o, acc_lse, acc_write, static_cast<float*>(out), sB, sH, sN,
         out_row0, n_total, lse_out);

@@ -37,6 +37,8 @@ cudaError_t launch_merge(int64_t rows, int B, int H, int D, int n_parts, const f
                          int64_t out_row0, int64_t n_total, float* lse_out, cudaStream_t st);
 cqs_status make_tmap_bf16(CUtensorMap* m, const void* base, int B, int H, int64_t rows, int D,
                           int64_t sB, int64_t sH, int64_t sN, int box_rows);
+int attn_rows_per_item(int D);
+int attn_k_box_rows(int D);
 void build_task_params_ext(const cqs_plan_t* p, const Task& T, int rows_per_item,
                            const int64_t* src_rows, const int64_t* dst_rows, TaskParams& tp);
 
@@ -110,7 +112,8 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
     for (int b = 0; b < S; ++b)
       for (int t = 0; t < 3; ++t) {
         cqs_status s2 = make_tmap_bf16(&maps[b][t], stage[b][t], d.B, d.H, Lh, d.D,
-                                       int64_t(d.H) * Lh * D, Lh * D, D, 128);
+                                       int64_t(d.H) * Lh * D, Lh * D, D,
+                                       t == 1 ? attn_k_box_rows(d.D) : 128);
         if (s2 != CQS_OK) return s2;
       }
   const int64_t sstr[4] = {int64_t(d.H) * Lh * D, Lh * D, D, 1};
@@ -134,6 +137,10 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
     }
     return CQS_OK;
   };
+
+  // Staging rows past a task's last staged segment are read by the last key tile of a segment
+  // (masked to P = 0) — they must be finite, since 0 * NaN = NaN in the P.V MMA.  Zero once.
+  CK(cudaMemsetAsync(ws + L.stage, 0, size_t(S) * L.stage_bytes_per_buf, st));
 
   if (j > 0) {  // host accumulator starts empty: lse = -inf
     CK(launch_fill(fb_l[0], F * BH, -INFINITY, st));
@@ -191,7 +198,8 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       CK(cudaEventRecord(ev_ready[b], sc.cs));
       CK(cudaStreamWaitEvent(st, ev_ready[b], 0));
       TaskParams tp;
-      build_task_params_ext(p, T, d.in_dtype == CQS_BF16 ? 256 : 32, src, dst, tp);
+      build_task_params_ext(p, T, d.in_dtype == CQS_BF16 ? attn_rows_per_item(d.D) : 32, src, dst,
+                            tp);
       if (d.in_dtype == CQS_BF16)
         CK(launch_attn_bf16(d.D, maps[b], tp, acc_o, acc_l, scale, st));
       else

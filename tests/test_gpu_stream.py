@@ -47,10 +47,13 @@ def check(out, lse, q, k, v, tol_o, tol_l):
 def test_streamed_bf16_budget_tiers(N, H, D):
     q, k, v = host_qkv(1, H, N, D, 31 + N, torch.bfloat16)
     d = cqs.make_desc(N=N, B=1, H=H, D=D, depth=-1, in_dtype="bf16", qkv_loc="host")
-    for (kk, j, nb) in [(2, 1, 2), (1, 0, 1), (3, 2, 2)]:
-        budget, _ = cqs.cqs_memory_model(d, kk, j, nb)
+    # (depth, budget tier) -> the exact tier the planner must pick (DESIGN §8 search order)
+    for (kk, j, nb, unlimited) in [(2, 1, 2, False), (1, 0, 2, True), (2, 2, 1, False),
+                                   (3, 2, 2, False)]:
+        budget = 0 if unlimited else cqs.cqs_memory_model(d, kk, j, nb)[0]
         out, lse, info, st, peak = run_streamed(q, k, v, budget, depth=kk)
-        assert info.depth == kk and info.acc_depth <= j
+        assert (info.depth, info.acc_depth, info.n_stage_buffers) == (kk, j, nb)
+        budget = budget or info.predicted_peak_bytes
         # peak is measured through torch's allocator, which rounds blocks up to 512 bytes
         assert info.predicted_peak_bytes <= budget and peak <= budget + 512
         assert st.bytes_h2d > 0 and st.tasks_run == info.my_tasks
@@ -72,7 +75,10 @@ def test_c3_streamed_16gib_sampled():
     peak device bytes <= budget; sampled rows vs the oracle."""
     B, H, N, D = 1, 32, 1_000_000, 128
     budget = 16 << 30
-    q, k, v = host_qkv(B, H, N, D, 20260419, torch.bfloat16)
+    # generated on the GPU (same integers as the CPU generator), kept in pinned host memory
+    q, k, v = (cqs_synth.torch_tensor((B, H, N, D), 20260419, nm, torch.bfloat16, "cuda")
+               .cpu().pin_memory() for nm in ("q", "k", "v"))
+    torch.cuda.empty_cache()
     out, lse, info, st, peak = run_streamed(q, k, v, budget)
     assert info.depth == 2 and peak <= budget + 512
     rng = np.random.default_rng(2)
