@@ -141,6 +141,11 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
   // Staging rows past a task's last staged segment are read by the last key tile of a segment
   // (masked to P = 0) — they must be finite, since 0 * NaN = NaN in the P.V MMA.  Zero once.
   CK(cudaMemsetAsync(ws + L.stage, 0, size_t(S) * L.stage_bytes_per_buf, st));
+  {
+    cudaEvent_t zeroed = sc.ev();   // the copy stream must not stage before the zeroing
+    CK(cudaEventRecord(zeroed, st));
+    CK(cudaStreamWaitEvent(sc.cs, zeroed, 0));
+  }
 
   if (j > 0) {  // host accumulator starts empty: lse = -inf
     CK(launch_fill(fb_l[0], F * BH, -INFINITY, st));
