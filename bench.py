@@ -90,6 +90,24 @@ class ClockSampler:
                 "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
 
 
+def ncu_traffic(kernel_prefix):
+    """dram read+write bytes per launch of the dominant kernel from the committed `ncu --set full`
+    summary (profiles/), or None."""
+    import glob
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_summary.json"))):
+        try:
+            for d in json.load(open(f)):
+                if d["kernel"].startswith(kernel_prefix) or kernel_prefix in d["kernel"]:
+                    rd, wr = d["dram__bytes_read.sum"], d["dram__bytes_write.sum"]
+                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+                    best = (float(rd["value"]) * scale[rd["unit"]] + float(wr["value"]) * scale[wr["unit"]],
+                            os.path.basename(f))
+        except Exception:
+            continue
+    return best
+
+
 def cpu_oracle_sample(cfg, seconds=10.0, max_rows=4096):
     """Time the oracle (fp64 dense rows, blockwise) on host cores: sampled query rows of head 0
     against all N keys.  Returns (TFLOP/s, rows, threads, secs)."""
@@ -285,6 +303,8 @@ def main():
         dist.destroy_process_group()
         return 0
     peaks, peak_src = load_peaks()
+    kname = "attn_bf16_sm100_2cta_kernel" if D == 128 else "attn_bf16_sm100_kernel<%d>" % D
+    traffic = ncu_traffic(kname)
     peak = peaks.get("bf16_tflops", 1645.9)
     value = flops / (ms * 1e-3) / 1e12
     # attention-kernel-only rate: this rank's algorithmic FLOPs / summed kernel durations (CUDA events)
@@ -307,9 +327,14 @@ def main():
         "tokens_per_s": N * B / (ms * 1e-3),
         "pct_tensor_peak": value / (world * peak),
         "roofline": {"bound": "tensor", "achieved": attn_tf, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (attn_tf / peak) if attn_tf else None, "traffic": None,
-                     "kernel": "attn_bf16_sm100_kernel<%d>" % D, "peak_source": peak_src,
-                     "flops_per_launch": flops / max(1, info.my_tasks)},
+                     "frac": (attn_tf / peak) if attn_tf else None,
+                     "traffic": traffic[0] if traffic else None,
+                     "traffic_source": traffic[1] if traffic else None,
+                     "kernel": kname, "peak_source": peak_src + " bf16_tflops (burst)",
+                     "frac_of_sustained": (attn_tf / peaks.get("bf16_tflops_sustained", peak))
+                     if attn_tf else None,
+                     "flops_per_launch": flops / max(1, info.my_tasks),
+                     "launches_per_step": info.my_tasks},
         "peak_mem": {"predicted_bytes": info.predicted_peak_bytes,
                      "torch_max_allocated": torch.cuda.max_memory_allocated(dev)},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,

@@ -52,8 +52,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
   uint64_t* kv_full = bars + 1;                        // leader: K/V half bytes of both CTAs
   uint64_t* kv_empty = kv_full + kStages;              // both: stage free (multicast commit)
   uint64_t* s_full = kv_empty + kStages;               // both: S_t ready (multicast commit)
-  uint64_t* p_full = s_full + 2;                       // leader: [tile][key half], 8 warps each
-  uint64_t* o_bar = p_full + 4;                        // both: PV_t retired (multicast commit)
+  uint64_t* p_full = s_full + 2;                       // leader: 8 softmax warps of the pair
+  uint64_t* o_bar = p_full + 2;                        // both: PV_t retired (multicast commit)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -82,8 +82,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       ptx::mbar_init(&s_full[t], 1);
-      ptx::mbar_init(&p_full[2 * t], 8);
-      ptx::mbar_init(&p_full[2 * t + 1], 8);
+      ptx::mbar_init(&p_full[t], 8);
       ptx::mbar_init(&o_bar[t], 1);
     }
     ptx::fence_barrier_init();
@@ -157,18 +156,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         }
         ptx::mma_commit_2sm(&s_full[t]);
       };
-      // O_t += P_t V over keys [64 h, 64 h + 64): issued as soon as that half of P is in TMEM,
-      // so the first half's MMAs overlap the softmax of the second half
-      auto issue_PV_half = [&](int t, int s, int h, bool acc) {
+      auto issue_PV = [&](int t, int s, bool acc) {
 #pragma unroll
-        for (int kk = 0; kk < kBN / 32; ++kk) {
-          const int ks = h * (kBN / 32) + kk;
+        for (int ks = 0; ks < kBN / 16; ++ks) {
           const uint64_t bd = ptx::smem_desc_sw128(skv + s * kStageBytes + ks * 16 * 128,
                                                    kBN * 128, 1024);
           ptx::mma_ts_2sm(tmem + colO[t], tmem + colS[t] + ks * 8, bd, idesc_pv,
                           (acc || ks > 0));
         }
-        if (h == 1) ptx::mma_commit_2sm(&o_bar[t]);
+        ptx::mma_commit_2sm(&o_bar[t]);
       };
       int it = 0;
       ptx::mbar_wait(q_full, 0);
@@ -191,11 +187,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         ++it;
         ptx::tc_fence_after();
         for (int t = 0; t < (two ? 2 : 1); ++t) {
-          for (int h = 0; h < 2; ++h) {
-            ptx::mbar_wait(&p_full[2 * t + h], j & 1);
-            ptx::tc_fence_after();
-            issue_PV_half(t, sV, h, j > 0);
-          }
+          ptx::mbar_wait(&p_full[t], j & 1);
+          ptx::tc_fence_after();
+          issue_PV(t, sV, j > 0);
           if (sKn >= 0) issue_S(t, sKn);
         }
         ptx::mma_commit_2sm(&kv_empty[sV]);
@@ -260,36 +254,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         }
         m = m_new;
         const uint64_t sc2 = ptx::f2(scale_log2, scale_log2), nm2 = ptx::f2(-m, -m);
+#pragma unroll
+        for (int i = 0; i < kBN / 2; ++i) {
+          float x0, x1;
+          ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
+          s[2 * i] = ptx::ex2(x0);
+          s[2 * i + 1] = ptx::ex2(x1);
+        }
         uint64_t rs2[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {       // key half h: exp2, row-sum, bf16 P -> TMEM, signal
-#pragma unroll
-          for (int i = h * kBN / 4; i < (h + 1) * kBN / 4; ++i) {
-            float x0, x1;
-            ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
-            s[2 * i] = ptx::ex2(x0);
-            s[2 * i + 1] = ptx::ex2(x1);
-            rs2[i & 3] = ptx::fadd2(rs2[i & 3], ptx::f2(s[2 * i], s[2 * i + 1]));
-          }
-#pragma unroll
-          for (int c = 2 * h; c < 2 * h + 2; ++c) {
-            uint32_t pk[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              pk[i] = ptx::pack_bf16(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]);
-            ptx::tmem_st16(tS + c * 16, pk);
-          }
-          ptx::tmem_st_wait();
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive_leader(&p_full[2 * t + h]);
-        }
+        for (int i = 0; i < kBN / 2; ++i)
+          rs2[i & 3] = ptx::fadd2(rs2[i & 3], ptx::f2(s[2 * i], s[2 * i + 1]));
         {
           const uint64_t rr = ptx::fadd2(ptx::fadd2(rs2[0], rs2[1]), ptx::fadd2(rs2[2], rs2[3]));
           float a0, a1;
           ptx::f2_split(rr, a0, a1);
           l += a0 + a1;
         }
+#pragma unroll
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]);
+          ptx::tmem_st16(tS + c * 16, pk);
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_leader(&p_full[t]);
       }
       // ---- epilogue ----
       ptx::mbar_wait(&o_bar[t], (n_kv - 1) & 1);
