@@ -154,30 +154,32 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer (one thread) =================
-    if (lane == 0) {
+    // ================= MMA issuer (whole warp, one elected lane issues) =================
+    {
       constexpr uint32_t idesc_qk = ptx::idesc_bf16(kBM, kBN, 0, 0);
       constexpr uint32_t idesc_pv = ptx::idesc_bf16(kBM, D, 0, 1);
-      const uint32_t sq = ptx::smem_u32(sQ), skv = ptx::smem_u32(sKV);
-      const uint32_t colS[2] = {C::kColS0, C::kColS1}, colO[2] = {C::kColO0, C::kColO1};
+      const uint64_t dq0 = ptx::smem_desc_sw128(ptx::smem_u32(sQ), 16, 1024);
+      const uint64_t dkv0 = ptx::smem_desc_sw128(ptx::smem_u32(sKV), 16, 1024);
+      const uint64_t dv0 = ptx::smem_desc_sw128(ptx::smem_u32(sKV), kBN * 128, 1024);
       auto issue_S = [&](int t, int s) {
+        const uint64_t qa = dq0 + uint64_t((t * C::kQBytes) >> 4);
+        const uint64_t kb = dkv0 + uint64_t((s * C::kKVBytes) >> 4);
+        const uint32_t d = tmem + (t ? C::kColS1 : C::kColS0);
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t off = (ks >> 2) * (kBM * 128) + (ks & 3) * 32;
-          const uint64_t ad = ptx::smem_desc_sw128(sq + t * C::kQBytes + off, 16, 1024);
-          const uint64_t bd = ptx::smem_desc_sw128(skv + s * C::kKVBytes + off, 16, 1024);
-          ptx::mma_ss(tmem + colS[t], ad, bd, idesc_qk, ks > 0);
+          const uint32_t off = ((ks >> 2) * (kBM * 128) + (ks & 3) * 32) >> 4;
+          ptx::mma_ss_elect(d, qa + off, kb + off, idesc_qk, ks > 0);
         }
-        ptx::mma_commit(&s_full[t]);
+        ptx::mma_commit_elect(&s_full[t]);
       };
       auto issue_PV = [&](int t, int s, bool acc) {
+        const uint64_t vb = dv0 + uint64_t((s * C::kKVBytes) >> 4);
+        const uint32_t d = tmem + (t ? C::kColO1 : C::kColO0), pa = tmem + (t ? C::kColS1 : C::kColS0);
 #pragma unroll
-        for (int ks = 0; ks < kBN / 16; ++ks) {
-          const uint64_t bd =
-              ptx::smem_desc_sw128(skv + s * C::kKVBytes + ks * 16 * 128, kBN * 128, 1024);
-          ptx::mma_ts(tmem + colO[t], tmem + colS[t] + ks * 8, bd, idesc_pv, (acc || ks > 0));
-        }
-        ptx::mma_commit(&o_bar[t]);
+        for (int ks = 0; ks < kBN / 16; ++ks)
+          ptx::mma_ts_elect(d, pa + ks * 8, vb + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
+                            (acc || ks > 0));
+        ptx::mma_commit_elect(&o_bar[t]);
       };
       int it = 0;
       ptx::mbar_wait(q_full, 0);
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       ptx::tc_fence_after();
       issue_S(0, sK0);
       if (two) issue_S(1, sK0);
-      ptx::mma_commit(&kv_empty[sK0]);
+      ptx::mma_commit_elect(&kv_empty[sK0]);
       for (int j = 0; j < n_kv; ++j) {
         int sKn = -1;
         if (j + 1 < n_kv) {
@@ -213,11 +215,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           issue_PV(t, sV, j > 0);
           if (sKn >= 0) issue_S(t, sKn);
         }
-        ptx::mma_commit(&kv_empty[sV]);
-        if (sKn >= 0) ptx::mma_commit(&kv_empty[sKn]);
+        ptx::mma_commit_elect(&kv_empty[sV]);
+        if (sKn >= 0) ptx::mma_commit_elect(&kv_empty[sKn]);
       }
       // drain: q_full's second phase completes when every MMA of this CTA has retired
-      ptx::mma_commit(q_full);
+      ptx::mma_commit_elect(q_full);
       ptx::mbar_wait(q_full, 1);
     }
   }

@@ -137,34 +137,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         if (j + 1 < n_kv) load_k();
         load_v();
       }
-    } else if (warp == 1 && lane == 0 && leader) {
-      // ================= MMA issuer (leader CTA, one thread) =================
+    } else if (warp == 1 && leader) {
+      // ================= MMA issuer (leader CTA; whole warp, one elected lane issues) =================
+      // Descriptors are precomputed: the smem start address lives in the low 14 bits (addr >> 4),
+      // so a byte offset is added as offset >> 4 (all offsets stay inside the 227 KB window).
       constexpr uint32_t idesc_qk = ptx::idesc_bf16(2 * kBM, kBN, 0, 0);   // M=256, N=128
       constexpr uint32_t idesc_pv = ptx::idesc_bf16(2 * kBM, D, 0, 1);     // M=256, N=128
-      const uint32_t sq = ptx::smem_u32(sQ), skv = ptx::smem_u32(sKV);
-      const uint32_t colS[2] = {kColS0, kColS1}, colO[2] = {kColO0, kColO1};
+      const uint64_t dq0 = ptx::smem_desc_sw128(ptx::smem_u32(sQ), 16, 1024);
+      const uint64_t dkv0 = ptx::smem_desc_sw128(ptx::smem_u32(sKV), 16, 1024);
+      const uint64_t dv0 = ptx::smem_desc_sw128(ptx::smem_u32(sKV), kBN * 128, 1024);
       auto issue_S = [&](int t, int s) {
+        const uint64_t qa = dq0 + uint64_t((t * kQBytes) >> 4);
+        const uint64_t kb = dkv0 + uint64_t((s * kStageBytes) >> 4);
+        const uint32_t d = tmem + (t ? kColS1 : kColS0);
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t kb = (ks & 3) * 32;
-          const uint64_t ad =
-              ptx::smem_desc_sw128(sq + t * kQBytes + (ks >> 2) * (kBM * 128) + kb, 16, 1024);
-          const uint64_t bd =
-              ptx::smem_desc_sw128(skv + s * kStageBytes + (ks >> 2) * (kKHalfRows * 128) + kb,
-                                   16, 1024);
-          ptx::mma_ss_2sm(tmem + colS[t], ad, bd, idesc_qk, ks > 0);
+          const uint32_t qo = ((ks >> 2) * (kBM * 128) + (ks & 3) * 32) >> 4;
+          const uint32_t ko = ((ks >> 2) * (kKHalfRows * 128) + (ks & 3) * 32) >> 4;
+          ptx::mma_ss_2sm_elect(d, qa + qo, kb + ko, idesc_qk, ks > 0);
         }
-        ptx::mma_commit_2sm(&s_full[t]);
+        ptx::mma_commit_2sm_elect(&s_full[t]);
       };
       auto issue_PV = [&](int t, int s, bool acc) {
+        const uint64_t vb = dv0 + uint64_t((s * kStageBytes) >> 4);
+        const uint32_t d = tmem + (t ? kColO1 : kColO0), pa = tmem + (t ? kColS1 : kColS0);
 #pragma unroll
-        for (int ks = 0; ks < kBN / 16; ++ks) {
-          const uint64_t bd = ptx::smem_desc_sw128(skv + s * kStageBytes + ks * 16 * 128,
-                                                   kBN * 128, 1024);
-          ptx::mma_ts_2sm(tmem + colO[t], tmem + colS[t] + ks * 8, bd, idesc_pv,
-                          (acc || ks > 0));
-        }
-        ptx::mma_commit_2sm(&o_bar[t]);
+        for (int ks = 0; ks < kBN / 16; ++ks)
+          ptx::mma_ts_2sm_elect(d, pa + ks * 8, vb + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
+                                (acc || ks > 0));
+        ptx::mma_commit_2sm_elect(&o_bar[t]);
       };
       int it = 0;
       ptx::mbar_wait(q_full, 0);
@@ -174,7 +175,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
       ptx::tc_fence_after();
       issue_S(0, sK0);
       if (two) issue_S(1, sK0);
-      ptx::mma_commit_2sm(&kv_empty[sK0]);
+      ptx::mma_commit_2sm_elect(&kv_empty[sK0]);
       for (int j = 0; j < n_kv; ++j) {
         int sKn = -1;
         if (j + 1 < n_kv) {
@@ -192,10 +193,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
           issue_PV(t, sV, j > 0);
           if (sKn >= 0) issue_S(t, sKn);
         }
-        ptx::mma_commit_2sm(&kv_empty[sV]);
-        if (sKn >= 0) ptx::mma_commit_2sm(&kv_empty[sKn]);
+        ptx::mma_commit_2sm_elect(&kv_empty[sV]);
+        if (sKn >= 0) ptx::mma_commit_2sm_elect(&kv_empty[sKn]);
       }
-      ptx::mma_commit_2sm(q_full);   // drain: all MMAs of the pair retired
+      ptx::mma_commit_2sm_elect(q_full);   // drain: all MMAs of the pair retired
       ptx::mbar_wait(q_full, 1);
     }
   } else {
