@@ -30,12 +30,13 @@ namespace cqs {
 constexpr int kAttnThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
 // column pairs (i mod 8) whose exp2 runs on the FMA pipe instead of MUFU
-// (measured on B200, C2 shape: at D=128 MUFU-only is fastest under the power cap — 958 vs 910
-// TFLOP/s with 3/8 emulated; at D=64 the MUFU bound dominates and 3/8 emulation gains ~1%)
+// (measured on B200 with the elected-issue kernels, C2 shape, under the 1 kW cap: at D=128 the
+// MUFU-only path and 1/8 emulation tie at ~1110 TFLOP/s and more emulation loses (power); at D=64,
+// where MUFU is the bound, 1/8 emulation is best: 703 vs 693 MUFU-only, 688 at 3/8, 680 at 4/8)
 #ifdef CQS_DBG_POLY_MASK
 template <int D> constexpr uint32_t kPolyMask = CQS_DBG_POLY_MASK;
 #else
-template <int D> constexpr uint32_t kPolyMask = D == 64 ? 0x25 : 0x0;
+template <int D> constexpr uint32_t kPolyMask = D == 64 ? 0x01 : 0x0;
 #endif
 
 template <int D>

@@ -33,6 +33,12 @@ constexpr int kStages = 8;
 constexpr int kSmemBytes = 2 * kQBytes + kStages * kStageBytes + 1024 + 512;
 constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 384;
 constexpr float kRescaleThreshold = 8.0f;
+// column pairs (i mod 8) whose exp2 runs as an FMA-pipe polynomial instead of MUFU.EX2
+#ifdef CQS_DBG_POLY_MASK
+constexpr uint32_t kPolyMask = CQS_DBG_POLY_MASK;
+#else
+constexpr uint32_t kPolyMask = 0x0;
+#endif
 }  // namespace pair
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
@@ -259,8 +265,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         for (int i = 0; i < kBN / 2; ++i) {
           float x0, x1;
           ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
-          s[2 * i] = ptx::ex2(x0);
-          s[2 * i + 1] = ptx::ex2(x1);
+          if ((kPolyMask >> (i & 7)) & 1) {
+            ptx::exp2_poly_pair(x0, x1);
+            if (2 * i >= valid) x0 = 0.f;   // masked tail columns (poly gives 2^-125)
+            if (2 * i + 1 >= valid) x1 = 0.f;
+          } else {
+            x0 = ptx::ex2(x0);
+            x1 = ptx::ex2(x1);
+          }
+          s[2 * i] = x0;
+          s[2 * i + 1] = x1;
         }
         uint64_t rs2[4] = {0, 0, 0, 0};
 #pragma unroll
