@@ -108,7 +108,7 @@ def ncu_traffic(kernel_prefix):
     return best
 
 
-def cpu_oracle_sample(cfg, seconds=10.0, max_rows=4096):
+def cpu_oracle_sample(cfg, seconds=12.0, max_rows=16384):
     """Time the oracle (fp64 dense rows, blockwise) on host cores: sampled query rows of head 0
     against all N keys.  Returns (TFLOP/s, rows, threads, secs)."""
     import numpy as np

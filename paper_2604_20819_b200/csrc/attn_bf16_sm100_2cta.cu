@@ -115,15 +115,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
                                q_row + t * 2 * kBM, hi, bi);
       int it = 0;
       auto stage_wait = [&](int s) {
+#ifdef CQS_DBG_NO_TMA_REFILL
+        if (it >= kStages) return false;
+#endif
         ptx::mbar_wait(&kv_empty[s], ((it / kStages) & 1) ^ 1);
         if (leader) ptx::mbar_arrive_expect_tx(&kv_full[s], 2 * kStageBytes);
+        return true;
       };
       KvCursor ck, cv;
       ck.init(&tp, kmask);
       cv.init(&tp, kmask);
       auto load_k = [&]() {   // keys [64 rank, 64 rank + 64) of the tile, both 64-col boxes
         const int s = it % kStages;
-        stage_wait(s);
+        if (stage_wait(s))
         for (int bx = 0; bx < 2; ++bx)
           ptx::tma_load_4d_2sm(sKV + s * kStageBytes + bx * kKHalfRows * 128, &tmK, &kv_full[s],
                                bx * 64, ck.row() + int(rank) * kKHalfRows, hi, bi);
@@ -132,7 +136,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
       };
       auto load_v = [&]() {   // head-dim columns [64 rank, 64 rank + 64) of all 128 keys
         const int s = it % kStages;
-        stage_wait(s);
+        if (stage_wait(s))
         ptx::tma_load_4d_2sm(sKV + s * kStageBytes, &tmV, &kv_full[s], int(rank) * 64, cv.row(),
                              hi, bi);
         cv.next();
@@ -186,15 +190,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         int sKn = -1;
         if (j + 1 < n_kv) {
           sKn = it % kStages;
+#ifdef CQS_DBG_NO_TMA_REFILL
+          if (it < kStages)
+#endif
           ptx::mbar_wait(&kv_full[sKn], (it / kStages) & 1);
           ++it;
         }
         const int sV = it % kStages;
+#ifdef CQS_DBG_NO_TMA_REFILL
+        if (it < kStages)
+#endif
         ptx::mbar_wait(&kv_full[sV], (it / kStages) & 1);
         ++it;
         ptx::tc_fence_after();
         for (int t = 0; t < (two ? 2 : 1); ++t) {
+#ifndef CQS_DBG_NO_PWAIT
           ptx::mbar_wait(&p_full[t], j & 1);
+#endif
           ptx::tc_fence_after();
           issue_PV(t, sV, j > 0);
           if (sKn >= 0) issue_S(t, sKn);
@@ -223,6 +235,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         cur.next();
         ptx::mbar_wait(&s_full[t], j & 1);
         ptx::tc_fence_after();
+#ifdef CQS_DBG_NO_PWAIT   // timing experiment only: softmax warps do nothing
+        break;
+#endif
+#ifdef CQS_DBG_SKIP_SOFTMAX   // timing experiment only: MMA/TMA pipeline without softmax math
+        if (j == 0) m = 0.f, l = 1.f;
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_leader(&p_full[t]);
+        continue;
+#endif
         uint32_t sr[kBN];
 #pragma unroll
         for (int c = 0; c < kBN / 32; ++c)
