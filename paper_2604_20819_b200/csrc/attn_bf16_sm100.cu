@@ -291,6 +291,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           l *= f;
         }
         m = m_new;
+        // MUFU ping-pong between the two softmax warpgroups (named barriers 1, 2; see the
+        // CTA-pair kernel)
+#ifdef CQS_PINGPONG
+        if (two && !(t == 0 && j == 0)) ptx::named_bar_sync(1 + t, 256);
+#endif
         // p = 2^(s*scale_log2 - m): packed FFMA2 for the argument, then MUFU.EX2 for most column
         // pairs and the FMA-pipe polynomial for the pairs selected by kPolyMask (load balance
         // between the 16/clk/SM MUFU and the issue slots)
@@ -312,6 +317,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           s[2 * i] = x0;
           s[2 * i + 1] = x1;
         }
+#ifdef CQS_PINGPONG
+        if (two && !(t == 1 && j == n_kv - 1)) ptx::named_bar_arrive(2 - t, 256);
+#endif
         if (valid < kBN) {
 #pragma unroll
           for (int c = 0; c < kBN; ++c)

@@ -41,6 +41,15 @@ constexpr uint32_t kPolyMask = 0x0;
 #endif
 }  // namespace pair
 
+#ifdef CQS_DBG_TIMING   // timing experiment only: per-role cycle accounting (tools/timing_probe.py)
+__device__ unsigned long long g_cqs_dbg[16];
+#define DBG_T0(v) const long long v = clock64()
+#define DBG_ADD(i, x) atomicAdd(&g_cqs_dbg[i], (unsigned long long)(x))
+#else
+#define DBG_T0(v)
+#define DBG_ADD(i, x)
+#endif
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
     attn_bf16_sm100_2cta_kernel(const __grid_constant__ CUtensorMap tmQ,
                                 const __grid_constant__ CUtensorMap tmK,   // box 64 x 64
@@ -178,6 +187,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         ptx::mma_commit_2sm_elect(&o_bar[t]);
       };
       int it = 0;
+#ifdef CQS_DBG_TIMING
+      long long mma_pwait = 0;
+#endif
+      DBG_T0(tm0);
       ptx::mbar_wait(q_full, 0);
       const int sK0 = it % kStages;
       ptx::mbar_wait(&kv_full[sK0], (it / kStages) & 1);
@@ -205,7 +218,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         ptx::tc_fence_after();
         for (int t = 0; t < (two ? 2 : 1); ++t) {
 #ifndef CQS_DBG_NO_PWAIT
+          DBG_T0(tw0);
           ptx::mbar_wait(&p_full[t], j & 1);
+#ifdef CQS_DBG_TIMING
+          DBG_T0(tw1);
+          mma_pwait += tw1 - tw0;
+#endif
 #endif
           ptx::tc_fence_after();
           issue_PV(t, sV, j > 0);
@@ -216,6 +234,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
       }
       ptx::mma_commit_2sm_elect(q_full);   // drain: all MMAs of the pair retired
       ptx::mbar_wait(q_full, 1);
+#ifdef CQS_DBG_TIMING
+      DBG_T0(tm1);
+      if (lane == 0) DBG_ADD(5, tm1 - tm0), DBG_ADD(6, n_kv), DBG_ADD(4, mma_pwait);
+#endif
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
@@ -228,13 +250,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
       const uint32_t tS = tmem + lane_base + (t ? kColS1 : kColS0);
       const uint32_t tO = tmem + lane_base + (t ? kColO1 : kColO0);
       float m = -INFINITY, l = 0.f;
+#ifdef CQS_DBG_TIMING
+      long long dc[12] = {};
+#endif
       KvCursor cur;
       cur.init(&tp, kmask);
       for (int j = 0; j < n_kv; ++j) {
         const int valid = cur.valid();
         cur.next();
+        DBG_T0(ts0);
         ptx::mbar_wait(&s_full[t], j & 1);
         ptx::tc_fence_after();
+        DBG_T0(ts1);
+#ifdef CQS_DBG_TIMING
+        dc[0] += ts1 - ts0, dc[2] += 1;
+#endif
 #ifdef CQS_DBG_NO_PWAIT   // timing experiment only: softmax warps do nothing
         break;
 #endif
@@ -250,19 +280,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         for (int c = 0; c < kBN / 32; ++c)
           ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
         ptx::tmem_ld_wait();
+        DBG_T0(tp_ld);
         float* s = reinterpret_cast<float*>(sr);
         if (valid < kBN) {
 #pragma unroll
           for (int c = 0; c < kBN; ++c)
             if (c >= valid) s[c] = -INFINITY;
         }
-        float mx4[4] = {s[0], s[1], s[2], s[3]};
+        // row max: 8 independent chains (3-input FMNMX3 each step), then a small tree
+        float mx8[8];
 #pragma unroll
-        for (int c = 4; c < kBN; c += 4) {
+        for (int u = 0; u < 8; ++u) mx8[u] = s[u];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) mx4[u] = fmaxf(mx4[u], s[c + u]);
+        for (int c = 8; c < kBN; c += 16) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], fmaxf(s[c + u], s[c + 8 + u]));
         }
-        const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale_log2;
+        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
         const float m_new = (j == 0 || mx > m + kRescaleThreshold) ? mx : m;
         const bool need = (j > 0) && (m_new != m);
         if (__any_sync(0xffffffffu, need)) {
@@ -282,44 +317,68 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
           l *= f;
         }
         m = m_new;
+        // Optional MUFU ping-pong between the two softmax warpgroups (named barriers 1 and 2,
+        // -DCQS_PINGPONG): forces the exp2 phases of tile 0 and tile 1 to alternate.  Measured
+        // slower (1071 vs 1107 TFLOP/s on C2): the per-tile S->P time is ~1.9k cycles against a
+        // 1k-cycle MMA chain, so strict alternation only adds waiting; off by default.
+        DBG_T0(tp_max);
+#ifdef CQS_PINGPONG
+        if (two && !(t == 0 && j == 0)) ptx::named_bar_sync(1 + t, 256);
+#endif
+        DBG_T0(tp_gate);
         const uint64_t sc2 = ptx::f2(scale_log2, scale_log2), nm2 = ptx::f2(-m, -m);
-#pragma unroll
-        for (int i = 0; i < kBN / 2; ++i) {
-          float x0, x1;
-          ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
-          if ((kPolyMask >> (i & 7)) & 1) {
-            ptx::exp2_poly_pair(x0, x1);
-            if (2 * i >= valid) x0 = 0.f;   // masked tail columns (poly gives 2^-125)
-            if (2 * i + 1 >= valid) x1 = 0.f;
-          } else {
-            x0 = ptx::ex2(x0);
-            x1 = ptx::ex2(x1);
-          }
-          s[2 * i] = x0;
-          s[2 * i + 1] = x1;
-        }
+        // fused per 32-column chunk: exp2 -> packed row-sum -> bf16 pack -> tcgen05.st, so the
+        // sums, packs and TMEM stores fill the issue slots between MUFU ops
         uint64_t rs2[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int i = 0; i < kBN / 2; ++i)
-          rs2[i & 3] = ptx::fadd2(rs2[i & 3], ptx::f2(s[2 * i], s[2 * i + 1]));
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int ii = 0; ii < 16; ++ii) {
+            const int i = 16 * c + ii;
+            float x0, x1;
+            ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
+            if ((kPolyMask >> (i & 7)) & 1) {
+              ptx::exp2_poly_pair(x0, x1);
+              if (2 * i >= valid) x0 = 0.f;   // masked tail columns (poly gives 2^-125)
+              if (2 * i + 1 >= valid) x1 = 0.f;
+            } else {
+              x0 = ptx::ex2(x0);
+              x1 = ptx::ex2(x1);
+            }
+            const uint64_t p2 = ptx::f2(x0, x1);
+            rs2[ii & 3] = ptx::fadd2(rs2[ii & 3], p2);
+            pk[ii] = ptx::pack_bf16(x0, x1);
+          }
+          ptx::tmem_st16(tS + c * 16, pk);
+        }
+        DBG_T0(tp_exp);
+#ifdef CQS_PINGPONG
+        if (two && !(t == 1 && j == n_kv - 1)) ptx::named_bar_arrive(2 - t, 256);
+#endif
         {
           const uint64_t rr = ptx::fadd2(ptx::fadd2(rs2[0], rs2[1]), ptx::fadd2(rs2[2], rs2[3]));
           float a0, a1;
           ptx::f2_split(rr, a0, a1);
           l += a0 + a1;
         }
-#pragma unroll
-        for (int c = 0; c < kBN / 32; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]);
-          ptx::tmem_st16(tS + c * 16, pk);
-        }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_leader(&p_full[t]);
+#ifdef CQS_DBG_TIMING
+        {
+          const long long tp_end = clock64();
+          dc[1] += tp_end - ts1, dc[7] += tp_ld - ts1, dc[8] += tp_max - tp_ld;
+          dc[9] += tp_gate - tp_max, dc[10] += tp_exp - tp_gate, dc[11] += tp_end - tp_exp;
+        }
+#endif
       }
+#ifdef CQS_DBG_TIMING
+      if (lane == 0)
+        for (int i = 0; i < 12; ++i)
+          if (i < 3 || i >= 7) DBG_ADD(i, dc[i]);
+#endif
       // ---- epilogue ----
       ptx::mbar_wait(&o_bar[t], (n_kv - 1) & 1);
       ptx::tc_fence_after();
@@ -353,6 +412,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
     ptx::tmem_dealloc_2sm(tmem, 512);
   }
 }
+
+#ifdef CQS_DBG_TIMING
+extern "C" int cqs_dbg_read(unsigned long long* out, int n) {
+  return int(cudaMemcpyFromSymbol(out, g_cqs_dbg, sizeof(unsigned long long) * n));
+}
+extern "C" int cqs_dbg_reset() {
+  unsigned long long z[16] = {};
+  return int(cudaMemcpyToSymbol(g_cqs_dbg, z, sizeof(z)));
+}
+#endif
 
 cudaError_t launch_attn_bf16_pair(const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
                                   float* acc_lse, float scale, cudaStream_t stream) {
