@@ -30,13 +30,14 @@ namespace cqs {
 constexpr int kAttnThreads = 384;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
 // column pairs (i mod 8) whose exp2 runs on the FMA pipe instead of MUFU
-// (measured on B200 with the elected-issue kernels, C2 shape, under the 1 kW cap: at D=128 the
-// MUFU-only path and 1/8 emulation tie at ~1110 TFLOP/s and more emulation loses (power); at D=64,
-// where MUFU is the bound, 1/8 emulation is best: 703 vs 693 MUFU-only, 688 at 3/8, 680 at 4/8)
+// (measured on B200, C2 shape, fused exp loop: MUFU-only is fastest at both head dims — D=64:
+// 750 TFLOP/s MUFU-only vs 716 at 1/4 of the pairs emulated, 658 at 1/2, 534 at 3/4; D=128 is
+// power-capped and emulation only lowers the clock.  The polynomial stays available for
+// experiments via -DCQS_DBG_POLY_MASK.)
 #ifdef CQS_DBG_POLY_MASK
 template <int D> constexpr uint32_t kPolyMask = CQS_DBG_POLY_MASK;
 #else
-template <int D> constexpr uint32_t kPolyMask = D == 64 ? 0x01 : 0x0;
+template <int D> constexpr uint32_t kPolyMask = 0x0;
 #endif
 
 template <int D>
@@ -263,14 +264,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           for (int c = 0; c < kBN; ++c)
             if (c >= valid) s[c] = -INFINITY;
         }
-        // row max with 4 independent chains (breaks the dependent FMNMX latency chain)
-        float mx4[4] = {s[0], s[1], s[2], s[3]};
+        // row max: 8 independent chains (3-input FMNMX3 each step), then a small tree
+        float mx8[8];
 #pragma unroll
-        for (int c = 4; c < kBN; c += 4) {
+        for (int u = 0; u < 8; ++u) mx8[u] = s[u];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) mx4[u] = fmaxf(mx4[u], s[c + u]);
+        for (int c = 8; c < kBN; c += 16) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], fmaxf(s[c + u], s[c + 8 + u]));
         }
-        float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * scale_log2;
+        float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
         const float m_new = (j == 0 || mx > m + kRescaleThreshold) ? mx : m;
         const bool need = (j > 0) && (m_new != m);
         if (__any_sync(0xffffffffu, need)) {
@@ -296,50 +300,44 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #ifdef CQS_PINGPONG
         if (two && !(t == 0 && j == 0)) ptx::named_bar_sync(1 + t, 256);
 #endif
-        // p = 2^(s*scale_log2 - m): packed FFMA2 for the argument, then MUFU.EX2 for most column
-        // pairs and the FMA-pipe polynomial for the pairs selected by kPolyMask (load balance
-        // between the 16/clk/SM MUFU and the issue slots)
+        // p = 2^(s*scale_log2 - m): packed FFMA2 for the argument, MUFU.EX2 for most column pairs
+        // and the FMA-pipe polynomial for the pairs in kPolyMask; fused per 32-column chunk with
+        // the packed row sum, the bf16 pack and the tcgen05.st of P
         const uint64_t sc2 = ptx::f2(scale_log2, scale_log2), nm2 = ptx::f2(-m, -m);
+        uint64_t rs2[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int i = 0; i < kBN / 2; ++i) {
-          float x0, x1;
-          ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int ii = 0; ii < 16; ++ii) {
+            const int i = 16 * c + ii;
+            float x0, x1;
+            ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
 #ifdef CQS_DBG_SKIP_EXP
-          if (true) {
-          } else
+            if (true) {
+            } else
 #endif
-          if ((kPolyMask<D> >> (i & 7)) & 1) {
-            ptx::exp2_poly_pair(x0, x1);
-          } else {
-            x0 = ptx::ex2(x0);
-            x1 = ptx::ex2(x1);
+            if ((kPolyMask<D> >> (i & 7)) & 1) {
+              ptx::exp2_poly_pair(x0, x1);
+              if (2 * i >= valid) x0 = 0.f;         // masked tail columns (poly gives 2^-125)
+              if (2 * i + 1 >= valid) x1 = 0.f;
+            } else {
+              x0 = ptx::ex2(x0);
+              x1 = ptx::ex2(x1);
+            }
+            rs2[ii & 3] = ptx::fadd2(rs2[ii & 3], ptx::f2(x0, x1));
+            pk[ii] = ptx::pack_bf16(x0, x1);
           }
-          s[2 * i] = x0;
-          s[2 * i + 1] = x1;
+          ptx::tmem_st16(tS + c * 16, pk);
         }
 #ifdef CQS_PINGPONG
         if (two && !(t == 1 && j == n_kv - 1)) ptx::named_bar_arrive(2 - t, 256);
 #endif
-        if (valid < kBN) {
-#pragma unroll
-          for (int c = 0; c < kBN; ++c)
-            if (c >= valid) s[c] = 0.f;
-        }
-        uint64_t rs2[4] = {0, 0, 0, 0};   // 4 independent packed partial row sums
-#pragma unroll
-        for (int i = 0; i < kBN / 2; ++i) rs2[i & 3] = ptx::fadd2(rs2[i & 3], ptx::f2(s[2 * i], s[2 * i + 1]));
         {
           const uint64_t r = ptx::fadd2(ptx::fadd2(rs2[0], rs2[1]), ptx::fadd2(rs2[2], rs2[3]));
           float a0, a1;
           ptx::f2_split(r, a0, a1);
           l += a0 + a1;
-        }
-#pragma unroll
-        for (int c = 0; c < kBN / 32; ++c) {   // P (bf16 pairs) over S's first 64 columns
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(s[32 * c + 2 * i], s[32 * c + 2 * i + 1]);
-          ptx::tmem_st16(tS + c * 16, pk);
         }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();

@@ -124,39 +124,43 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Finalize (no parts): O = acc_o (0 where acc_lse = -inf), lse = acc_lse; pure streaming copy+cast.
+// Finalize (no parts): O = acc_o (0 where acc_lse = -inf), lse = acc_lse; a pure streaming
+// copy + cast.  Thread -> (unit, float4 column) with D4 = D/4 a power of two (shift), 32-bit index
+// math when the unit count fits (the 64-bit divisions of a flat int64 index ran on the XU pipe
+// and held this kernel at 62% of the HBM roofline).
 constexpr int kFinVec = 4;
-template <typename OutT>
+template <typename OutT, typename Idx>
 __global__ void __launch_bounds__(256)
-    finalize_kernel(int64_t rows, int BH, int H, int D, const float* __restrict__ acc_o,
+    finalize_kernel(Idx nunits, int BH, int H, int d4_shift, const float* __restrict__ acc_o,
                     const float* __restrict__ acc_lse, OutT* __restrict__ out, int64_t sB,
                     int64_t sH, int64_t sN, int64_t out_row0, int64_t n_total,
                     float* __restrict__ lse_out) {
-  const int D4 = D >> 2;
-  const int64_t n4 = rows * BH * D4;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; b < n4; b += stride * kFinVec) {
+  const Idx D4 = Idx(1) << d4_shift;
+  const Idx n4 = nunits << d4_shift;
+  const Idx stride = Idx(gridDim.x) * blockDim.x;
+  for (Idx b = Idx(blockIdx.x) * blockDim.x + threadIdx.x; b < n4; b += stride * kFinVec) {
     float4 v[kFinVec];
     float l[kFinVec];
 #pragma unroll
     for (int u = 0; u < kFinVec; ++u) {
-      const int64_t f = b + u * stride;
+      const Idx f = b + u * stride;
       if (f < n4) {
         v[u] = reinterpret_cast<const float4*>(acc_o)[f];
-        l[u] = acc_lse[f / D4];
+        l[u] = acc_lse[f >> d4_shift];
       }
     }
 #pragma unroll
     for (int u = 0; u < kFinVec; ++u) {
-      const int64_t f = b + u * stride;
+      const Idx f = b + u * stride;
       if (f >= n4) continue;
-      const int64_t unit = f / D4;
-      const int d = int(f - unit * D4) * 4;
+      const Idx unit = f >> d4_shift;
+      const int d = int(f & (D4 - 1)) * 4;
       if (l[u] == -INFINITY) v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      const int64_t r = unit / BH;
-      const int p = int(unit - r * BH);
-      store4(out + int64_t(p / H) * sB + int64_t(p % H) * sH + (out_row0 + r) * sN + d, v[u]);
-      if (d == 0 && lse_out) lse_out[int64_t(p) * n_total + out_row0 + r] = l[u];
+      const Idx r = unit / Idx(BH);
+      const int p = int(unit - r * Idx(BH));
+      const int bb = p / H, hh = p - bb * H;
+      store4(out + int64_t(bb) * sB + int64_t(hh) * sH + (out_row0 + int64_t(r)) * sN + d, v[u]);
+      if (d == 0 && lse_out) lse_out[int64_t(p) * n_total + out_row0 + int64_t(r)] = l[u];
     }
   }
 }
@@ -184,17 +188,21 @@ cudaError_t launch_merge(int64_t rows, int B, int H, int D, int n_parts, const f
   const int64_t sB = out ? out_strides[0] : 0, sH = out ? out_strides[1] : 0,
                 sN = out ? out_strides[2] : 0;
   const bool bf = out && out_dtype == CQS_BF16;
-  if (n_parts == 0 && acc_o && !acc_write && out) {
+  if (n_parts == 0 && acc_o && !acc_write && out && (D & (D - 1)) == 0) {
+    int shift = 0;
+    while ((4 << shift) < D) ++shift;
     const int64_t n4 = nunits * (D / 4);
     const int64_t blocks = std::min<int64_t>((n4 + 256 * kFinVec - 1) / (256 * kFinVec), 148 * 32);
-    if (bf)
-      finalize_kernel<__nv_bfloat16><<<unsigned(blocks), 256, 0, st>>>(
-          rows, BH, H, D, acc_o, acc_lse, static_cast<__nv_bfloat16*>(out), sB, sH, sN, out_row0,
-          n_total, lse_out);
-    else
-      finalize_kernel<float><<<unsigned(blocks), 256, 0, st>>>(
-          rows, BH, H, D, acc_o, acc_lse, static_cast<float*>(out), sB, sH, sN, out_row0, n_total,
-          lse_out);
+    const bool small = n4 + int64_t(blocks) * 256 * kFinVec < (int64_t(1) << 31);
+#define CQS_FIN(T, I)                                                                           \
+  finalize_kernel<T, I><<<unsigned(blocks), 256, 0, st>>>(                                      \
+      I(nunits), BH, H, shift, acc_o, acc_lse, static_cast<T*>(out), sB, sH, sN, out_row0,      \
+      n_total, lse_out)
+    if (bf && small) CQS_FIN(__nv_bfloat16, uint32_t);
+    else if (bf) CQS_FIN(__nv_bfloat16, int64_t);
+    else if (small) CQS_FIN(float, uint32_t);
+    else CQS_FIN(float, int64_t);
+#undef CQS_FIN
     return cudaGetLastError();
   }
   const int64_t blocks = std::min<int64_t>((nunits + 8 * kUnits - 1) / (8 * kUnits), 148 * 32);
