@@ -180,6 +180,8 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1: merge over peer memory in one kernel (p2p) or NCCL all-to-all + merge")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.impl == "reference":
@@ -194,10 +196,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CQS_SAME_DEVICE=1 + CQS_DIST_BACKEND=gloo: exercise the multi-rank code path with all ranks
+    # on one GPU (validation only; NCCL refuses two ranks per device)
+    if os.environ.get("CQS_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("CQS_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         cfg["depth"] = max(cfg["depth"], 2)   # 49 tasks: LPT balance across ranks
     N, B, H, D, depth = cfg["N"], cfg["B"], cfg["H"], cfg["D"], cfg["depth"]
     bf = cfg["dtype"] == "bf16"
@@ -219,6 +229,7 @@ def main():
         base = ws.data_ptr()
         acc_o = ws[ao - base: ao - base + N * BH * D * 4].view(torch.float32).view(N, BH * D)
         acc_l = ws[al - base: al - base + N * BH * 4].view(torch.float32).view(N, BH)
+        px = cdist.PeerExchange(p0, ws, N, B, H, D, world, rank) if args.exchange == "p2p" else None
 
     flops = 4.0 * N * N * D * BH
 
@@ -226,7 +237,9 @@ def main():
         p = cqs.cqs_plan(**desc_kw)                      # a1: CQS Divide planning (host C++)
         st = cqs.cqs_attention_forward(p, q, k, v, out, lse if world == 1 else None, 0.0, 0, ws,
                                        None, stream, stats=with_stats)
-        if world > 1:                                     # a5: one exchange + R-way merge
+        if world > 1 and args.exchange == "p2p":      # a5: exchange + merge over NVLink, 1 kernel
+            px.merge(out, lse, stream)
+        elif world > 1:                                   # a5: NCCL all-to-all + R-way merge
             ro, rl, r0, nr = cdist.exchange_partials(acc_o, acc_l, N, world, rank)
             cdist.merge_shard_gpu(ro, rl, world, nr, B, H, D, out, lse, r0, N, stream)
         return st
@@ -254,10 +267,11 @@ def main():
             dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        rdev = dev if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([ms], device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        launches_t = torch.tensor([launches], device=dev, dtype=torch.float64)
+        launches_t = torch.tensor([launches], device=rdev, dtype=torch.float64)
         dist.all_reduce(launches_t)
         launches = int(launches_t.item())
 
@@ -323,7 +337,8 @@ def main():
         "config": {"workload": cfg["desc"], "N": N, "B": B, "H": H, "D": D, "depth": info.depth,
                    "tasks": info.n_tasks, "l2": "inputs %.1f GB >> 126 MB L2 (no flush needed)"
                    % (3 * q.numel() * q.element_size() / 1e9),
-                   "parallelism": "task-sharded x%d" % world},
+                   "parallelism": "task-sharded x%d" % world,
+                   "exchange": args.exchange if world > 1 else None},
         "tokens_per_s": N * B / (ms * 1e-3),
         "pct_tensor_peak": value / (world * peak),
         "roofline": {"bound": "tensor", "achieved": attn_tf, "peak": peak, "unit": "TFLOP/s",

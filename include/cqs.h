@@ -176,6 +176,19 @@ cqs_status cqs_merge(int64_t rows, int32_t B, int32_t H, int32_t D, int32_t n_pa
                      float* acc_lse, void* out, cqs_dtype out_dtype, const int64_t out_strides[4],
                      int64_t out_row0, int64_t n_total, float* lse_out, void* stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * Peer-memory plumbing for the multi-GPU exchange (one process per GPU).  The final
+ * merge reads every rank's partial accumulator directly over NVLink: each rank exports its
+ * workspace with cqs_ipc_handle, peers map it with cqs_ipc_open, and cqs_merge is then launched
+ * with peer device pointers as its parts (one kernel = exchange + R-way merge).
+ * --------------------------------------------------------------------------------------------- */
+/* handle (64 bytes, caller-owned) of the device allocation containing dev_ptr, and dev_ptr's byte
+ * offset inside it.  Errors: CQS_E_INVALID (NULL), CQS_E_CUDA (not an exportable allocation). */
+cqs_status cqs_ipc_handle(const void* dev_ptr, void* handle, uint64_t* offset);
+/* Map a peer's allocation (from cqs_ipc_handle) into this process; *base is its base address. */
+cqs_status cqs_ipc_open(const void* handle, void** base);
+cqs_status cqs_ipc_close(void* base);
+
 const char* cqs_last_error(void);
 int32_t cqs_abi_version(void);
 

@@ -29,7 +29,8 @@ STATUS_NAMES = {0: "CQS_OK", 1: "CQS_E_VERIFY", 2: "CQS_E_INFEASIBLE", 3: "CQS_E
 ABI_SYMBOLS = ("cqs_plan", "cqs_plan_info", "cqs_plan_task", "cqs_plan_serialize",
                "cqs_plan_destroy", "cqs_memory_model", "cqs_forward_workspace_size",
                "cqs_attention_forward", "cqs_partial_view", "cqs_shard_rows", "cqs_merge",
-               "cqs_last_error", "cqs_abi_version")
+               "cqs_ipc_handle", "cqs_ipc_open", "cqs_ipc_close", "cqs_last_error",
+               "cqs_abi_version")
 
 
 class CqsError(RuntimeError):
@@ -101,6 +102,9 @@ def lib():
         L.cqs_merge.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                 C.POINTER(P), C.POINTER(P), P, P, P, C.c_int,
                                 C.POINTER(C.c_int64), C.c_int64, C.c_int64, P, P]
+        L.cqs_ipc_handle.argtypes = [P, P, C.POINTER(C.c_uint64)]
+        L.cqs_ipc_open.argtypes = [P, C.POINTER(P)]
+        L.cqs_ipc_close.argtypes = [P]
         L.cqs_last_error.restype = C.c_char_p
         L.cqs_abi_version.restype = C.c_int32
         for name in ABI_SYMBOLS:
@@ -237,18 +241,41 @@ def cqs_shard_rows(N, world, rank):
     return a.value, n.value
 
 
+def _addr(x):
+    return x if isinstance(x, int) else x.data_ptr()
+
+
 def cqs_merge(rows, B, H, D, part_o, part_lse, acc_o=None, acc_lse=None, out=None,
               out_row0=0, n_total=None, lse_out=None, stream=None):
-    """part_o / part_lse: lists of fp32 device tensors ([rows, B*H, D] / [rows, B*H])."""
+    """part_o / part_lse: fp32 device tensors ([rows, B*H, D] / [rows, B*H]) or raw device
+    addresses (e.g. peer memory mapped with cqs_ipc_open)."""
     n = len(part_o)
-    po = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in part_o])
-    pl = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in part_lse])
+    po = (C.c_void_p * max(n, 1))(*[_addr(t) for t in part_o])
+    pl = (C.c_void_p * max(n, 1))(*[_addr(t) for t in part_lse])
     import torch
     od = CQS_BF16 if (out is not None and out.dtype == torch.bfloat16) else CQS_F32
     _check(lib().cqs_merge(int(rows), B, H, D, n, po, pl, _ptr(acc_o), _ptr(acc_lse), _ptr(out), od,
                            _i64x4(out.stride()) if out is not None else None, int(out_row0),
                            int(n_total if n_total is not None else rows), _ptr(lse_out),
                            _stream_ptr(stream)))
+
+
+def cqs_ipc_handle(dev_ptr: int):
+    """(64-byte handle, byte offset) of the device allocation containing dev_ptr."""
+    h = C.create_string_buffer(64)
+    off = C.c_uint64()
+    _check(lib().cqs_ipc_handle(C.c_void_p(dev_ptr), h, C.byref(off)))
+    return h.raw, off.value
+
+
+def cqs_ipc_open(handle: bytes) -> int:
+    base = C.c_void_p()
+    _check(lib().cqs_ipc_open(C.create_string_buffer(handle, 64), C.byref(base)))
+    return base.value
+
+
+def cqs_ipc_close(base: int):
+    _check(lib().cqs_ipc_close(C.c_void_p(base)))
 
 
 def attention(q, k, v, depth=1, budget_bytes=0, out_dtype=None, scale=0.0, want_lse=True,

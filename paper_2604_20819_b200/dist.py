@@ -12,7 +12,8 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import cqs_shard_rows
+from . import cqs_ipc_close, cqs_ipc_handle, cqs_ipc_open, cqs_merge, cqs_partial_view, \
+    cqs_shard_rows
 
 
 def shard_spans(N: int, world: int):
@@ -46,7 +47,56 @@ def split_parts(recv_o: torch.Tensor, recv_l: torch.Tensor, world: int, rows: in
 def merge_shard_gpu(recv_o, recv_l, world, rows, B, H, D, out, lse, row0, N, stream=None):
     """R-way LSE merge of the received partials into rows [row0, row0+rows) of out / lse
     (cqs_merge kernel on the GPU)."""
-    from . import cqs_merge
     po, pl = split_parts(recv_o, recv_l, world, rows)
     cqs_merge(rows, B, H, D, po, pl, out=out, out_row0=row0, n_total=N, lse_out=lse,
               stream=stream)
+
+
+class PeerExchange:
+    """Exchange + merge in ONE kernel over peer memory (NVLink / NVSwitch): every rank maps all
+    ranks' partial accumulators (CUDA IPC, handles swapped once through torch.distributed) and
+    launches cqs_merge with the peers' shard rows as its parts, reading them directly over the
+    links — no staging all-to-all, no second pass.  The workspace must stay allocated (and at the
+    same address) for the object's lifetime; mappings are reused across steps."""
+
+    def __init__(self, plan, ws, N, B, H, D, world, rank, group=None):
+        self.N, self.B, self.H, self.D, self.world, self.rank = N, B, H, D, world, rank
+        self.group = group
+        ao, al = cqs_partial_view(plan, ws)
+        mine = (cqs_ipc_handle(ao), cqs_ipc_handle(al))
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self.opened = []
+        self.po, self.pl = [], []
+        self.row0, self.rows = cqs_shard_rows(N, world, rank)
+        BH = B * H
+        for r in range(world):
+            if r == rank:
+                bo, bl = ao, al
+            else:
+                (ho, oo), (hl, ol) = allh[r]
+                base_o = cqs_ipc_open(ho)
+                self.opened.append(base_o)
+                if hl == ho:                      # same allocation (one workspace tensor)
+                    base_l = base_o
+                else:
+                    base_l = cqs_ipc_open(hl)
+                    self.opened.append(base_l)
+                bo, bl = base_o + oo, base_l + ol
+            self.po.append(bo + self.row0 * BH * D * 4)
+            self.pl.append(bl + self.row0 * BH * 4)
+
+    def merge(self, out, lse, stream=None):
+        """Call after every rank's forward has been issued on its stream: barrier (all partials
+        complete), one merge kernel over peer memory, barrier (peers done reading)."""
+        torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+        dist.barrier(group=self.group)
+        cqs_merge(self.rows, self.B, self.H, self.D, self.po, self.pl, out=out, out_row0=self.row0,
+                  n_total=self.N, lse_out=lse, stream=stream)
+        torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+        dist.barrier(group=self.group)
+
+    def close(self):
+        for b in self.opened:
+            cqs_ipc_close(b)
+        self.opened = []

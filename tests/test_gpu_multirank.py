@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, N, H, D, depth, outdir):
+def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import cqs_synth
@@ -45,8 +45,14 @@ def _worker(rank, world, port, N, H, D, depth, outdir):
     acc_o = ws[ao - base: ao - base + N * H * D * 4].view(torch.float32).view(N, H * D)
     acc_l = ws[al - base: al - base + N * H * 4].view(torch.float32).view(N, H)
     torch.cuda.synchronize()
-    ro, rl, row0, rows = cdist.exchange_partials(acc_o.cpu(), acc_l.cpu(), N, world, rank)
-    cdist.merge_shard_gpu(ro.cuda(), rl.cuda(), world, rows, 1, H, D, out, lse, row0, N)
+    if mode == "p2p":   # exchange + merge in one kernel over peer (IPC-mapped) memory
+        px = cdist.PeerExchange(plan, ws, N, 1, H, D, world, rank)
+        row0, rows = px.row0, px.rows
+        px.merge(out, lse)
+        px.close()
+    else:
+        ro, rl, row0, rows = cdist.exchange_partials(acc_o.cpu(), acc_l.cpu(), N, world, rank)
+        cdist.merge_shard_gpu(ro.cuda(), rl.cuda(), world, rows, 1, H, D, out, lse, row0, N)
     torch.cuda.synchronize()
     np.save(os.path.join(outdir, "o%d.npy" % rank), out[0, :, row0:row0 + rows].float().cpu().numpy())
     np.save(os.path.join(outdir, "l%d.npy" % rank), lse[0, :, row0:row0 + rows].cpu().numpy())
@@ -54,12 +60,13 @@ def _worker(rank, world, port, N, H, D, depth, outdir):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("mode", ["gloo", "p2p"])
 @pytest.mark.parametrize("N,depth", [(3000, 2), (2401, 3)])
-def test_two_ranks_one_gpu(N, depth, tmp_path):
+def test_two_ranks_one_gpu(N, depth, mode, tmp_path):
     import cqs_synth
     from oracle import cqs_oracle as O
     world, H, D = 2, 2, 128
-    mp.start_processes(_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path)),
+    mp.start_processes(_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path), mode),
                        nprocs=world, start_method="spawn")
     q, k, v = cqs_synth.torch_qkv(1, H, N, D, 4242, dtype=torch.bfloat16)
     Od, ld = O.dense_attention(*(t.double().numpy() for t in (q, k, v)))
