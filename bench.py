@@ -247,6 +247,7 @@ def main():
     for _ in range(args.warmup):
         step(False)
     torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats(dev)   # peak over the timed region: caller tensors + ws
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -266,6 +267,7 @@ def main():
         if world > 1:
             dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
+    timed_peak = torch.cuda.max_memory_allocated(dev)
     if world > 1:
         rdev = dev if dist.get_backend() == "nccl" else "cpu"
         t = torch.tensor([ms], device=rdev)
@@ -351,7 +353,9 @@ def main():
                      "flops_per_launch": flops / max(1, info.my_tasks),
                      "launches_per_step": info.my_tasks},
         "peak_mem": {"predicted_bytes": info.predicted_peak_bytes,
-                     "torch_max_allocated": torch.cuda.max_memory_allocated(dev)},
+                     "measured_bytes_timed_region": timed_peak,
+                     "note": "all device bytes live during the timed steps (Q/K/V/O/lse + "
+                             "workspace; torch caching-allocator view, no budget set for C2)"},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
     }
     print(json.dumps(line))

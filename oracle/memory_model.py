@@ -13,7 +13,12 @@ from __future__ import annotations
 
 from oracle import cqs_oracle as O
 
-FLUSH_ROWS = 65536
+FLUSH_BYTES = 256 << 20   # two flush buffers of ~FLUSH_BYTES each
+
+
+def flush_rows(acc_rows, BH, D):
+    f = FLUSH_BYTES // (BH * (D + 1) * 4)
+    return min(max(f, 1024), 65536, acc_rows)
 
 
 def _a256(x):
@@ -51,7 +56,7 @@ def workspace_bytes(N, BH, D, e_in, streamed, out_host, staged_rows, acc_rows, n
     if streamed:
         b += nbuf * 3 * _a256(BH * staged_rows * D * e_in)
     if streamed or out_host:
-        F = min(acc_rows, FLUSH_ROWS)
+        F = flush_rows(acc_rows, BH, D)
         b += 2 * (_a256(F * BH * D * 4) + _a256(F * BH * 4))
     return b
 

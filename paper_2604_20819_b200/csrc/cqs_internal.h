@@ -56,7 +56,14 @@ struct WsLayout {
 };
 WsLayout ws_layout(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_rows,
                    int32_t n_stage_buffers);
-constexpr int64_t kFlushRows = 65536;
+// Flush buffers (streamed mode): two buffers of F rows x B*H x (D+1) fp32 with
+// F = clamp(kFlushBytes / (B*H*(D+1)*4), 1024, 65536), never more than the accumulator rows.
+constexpr int64_t kFlushBytes = 256ll << 20;
+inline int64_t flush_rows(int64_t acc_rows, int64_t BH, int64_t D) {
+  int64_t f = kFlushBytes / (BH * (D + 1) * 4);
+  f = f < 1024 ? 1024 : (f > 65536 ? 65536 : f);
+  return f < acc_rows ? f : acc_rows;
+}
 // Segments of the depth-`depth` subsequence selected by quorum[0..depth) (Alg. 3).
 bool build_segments(int64_t N, int c, const std::vector<int32_t>& I, const int32_t* quorum,
                     int depth, std::vector<Seg>& out);

@@ -49,7 +49,7 @@ WsLayout ws_layout(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_rows
   }
   w.flush = off;
   if (d.qkv_loc == CQS_LOC_PINNED_HOST || d.out_loc == CQS_LOC_PINNED_HOST) {
-    const uint64_t F = uint64_t(std::min<int64_t>(acc_rows, kFlushRows));
+    const uint64_t F = uint64_t(flush_rows(acc_rows, int64_t(BH), int64_t(D)));
     off += 2 * (align256(F * BH * D * 4) + align256(F * BH * 4));
   }
   w.total = off;

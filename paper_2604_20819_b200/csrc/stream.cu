@@ -50,11 +50,13 @@ void build_task_params_ext(const cqs_plan_t* p, const Task& T, int rows_per_item
 
 namespace {
 struct Scoped {
-  cudaStream_t cs = nullptr;
+  cudaStream_t cs = nullptr, fh = nullptr, fd = nullptr;
   std::vector<cudaEvent_t> evs;
   ~Scoped() {
     for (auto e : evs) cudaEventDestroy(e);
     if (cs) cudaStreamDestroy(cs);
+    if (fh) cudaStreamDestroy(fh);
+    if (fd) cudaStreamDestroy(fd);
   }
   cudaEvent_t ev() {
     cudaEvent_t e;
@@ -85,7 +87,7 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
   uint8_t* stage[2][3];
   for (int b = 0; b < S; ++b)
     for (int t = 0; t < 3; ++t) stage[b][t] = ws + L.stage + b * L.stage_bytes_per_buf + t * tens_bytes;
-  const int64_t F = std::min<int64_t>(Lacc, kFlushRows);
+  const int64_t F = flush_rows(Lacc, BH, D);
   const uint64_t fbo = align256(uint64_t(F * BH * D * 4)), fbl = align256(uint64_t(F * BH * 4));
   float* fb_o[2];
   float* fb_l[2];
@@ -101,6 +103,14 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
 
   Scoped sc;
   CK(cudaStreamCreateWithFlags(&sc.cs, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&sc.fh, cudaStreamNonBlocking));   // flush H2D
+  CK(cudaStreamCreateWithFlags(&sc.fd, cudaStreamNonBlocking));   // flush / output D2H
+  // flush buffer b: loaded (H2D done) -> merged (kernel done) -> free (D2H done)
+  cudaEvent_t fb_loaded[2] = {sc.ev(), sc.ev()}, fb_merged[2] = {sc.ev(), sc.ev()},
+              fb_free[2] = {sc.ev(), sc.ev()};
+  int fb_next = 0;
+  cudaEvent_t flush_done = sc.ev();
+  bool flushed_once = false;
   cudaEvent_t ev_ready[2] = {sc.ev(), sc.ev()}, ev_free[2] = {sc.ev(), sc.ev()};
   bool buf_used[2] = {false, false};
   uint64_t h2d = 0, d2h = 0;
@@ -118,23 +128,37 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       }
   const int64_t sstr[4] = {int64_t(d.H) * Lh * D, Lh * D, D, 1};
 
-  // final O/lse for rows [r0, r0+n) from an fp32 [n][BH][D] + [n][BH] source on the device
-  auto emit_final = [&](const float* src_o, const float* src_l, int64_t r0, int64_t n) -> cqs_status {
+  // Flush-buffer pipeline (two buffers alternate): H2D on sc.fh, kernel on st, D2H on sc.fd, so
+  // chunk i+1's upload, chunk i's merge and chunk i-1's download overlap.
+  auto fb_acquire = [&]() -> int {
+    const int b = fb_next;
+    fb_next ^= 1;
+    cudaStreamWaitEvent(sc.fh, fb_free[b], 0);   // never-recorded events are no-ops
+    cudaStreamWaitEvent(st, fb_free[b], 0);
+    return b;
+  };
+  // final O/lse for rows [r0, r0+n) from an fp32 [n][BH][D] + [n][BH] source on the device,
+  // staged as [BH][F][D] out + [BH][F] lse in flush buffer `b` and downloaded on sc.fd
+  auto emit_final = [&](int b, const float* src_o, const float* src_l, int64_t r0,
+                        int64_t n) -> cqs_status {
     const int64_t ostr[4] = {int64_t(d.H) * F * D, F * D, D, 1};
-    void* ob = fb_o[1];
-    float* lb = fb_l[1];
+    void* ob = fb_o[b];
+    float* lb = fb_l[b];
     CK(launch_merge(n, d.B, d.H, d.D, 0, nullptr, nullptr, const_cast<float*>(src_o),
                     const_cast<float*>(src_l), false, ob, d.out_dtype, ostr, 0, F, lb, st));
     ++launches;
+    CK(cudaEventRecord(fb_merged[b], st));
+    CK(cudaStreamWaitEvent(sc.fd, fb_merged[b], 0));
     CK(cudaMemcpy2DAsync(static_cast<uint8_t*>(out) + r0 * D * e_out, size_t(N * D * e_out), ob,
                          size_t(F * D * e_out), size_t(n * D * e_out), size_t(BH),
-                         cudaMemcpyDeviceToHost, st));
+                         cudaMemcpyDeviceToHost, sc.fd));
     d2h += uint64_t(n * D * e_out * BH);
     if (lse) {
       CK(cudaMemcpy2DAsync(lse + r0, size_t(N * 4), lb, size_t(F * 4), size_t(n * 4), size_t(BH),
-                           cudaMemcpyDeviceToHost, st));
+                           cudaMemcpyDeviceToHost, sc.fd));
       d2h += uint64_t(n * 4 * BH);
     }
+    CK(cudaEventRecord(fb_free[b], sc.fd));
     return CQS_OK;
   };
 
@@ -154,6 +178,8 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       const int64_t n = std::min(F, N - r);
       CK(cudaMemcpyAsync(hacc_l + r * BH, fb_l[0], size_t(n * BH * 4), cudaMemcpyDeviceToHost, st));
     }
+    CK(cudaEventRecord(fb_free[0], st));     // flush buffer 0 and the host rows are settled
+    CK(cudaStreamWaitEvent(sc.fh, fb_free[0], 0));
   }
 
   std::vector<Seg> node;
@@ -218,47 +244,70 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       ++run;
     }
 
-    // ---- flush the subtree accumulator ----
+    // ---- flush the subtree accumulator (pipelined over the two flush buffers) ----
+    if (j > 0 && flushed_once) CK(cudaStreamWaitEvent(sc.fh, flush_done, 0));  // host rows settled
     for (size_t s = 0; s < node.size(); ++s) {
       for (int64_t c0 = 0; c0 < node[s].len; c0 += F) {
         const int64_t n = std::min(F, node[s].len - c0);
         const int64_t grow = node[s].start + c0, lrow = node_off[s] + c0;
+        const int b = fb_acquire();
         if (j == 0) {
-          cqs_status s2 = emit_final(acc_o + lrow * BH * D, acc_l + lrow * BH, grow, n);
+          cqs_status s2 = emit_final(b, acc_o + lrow * BH * D, acc_l + lrow * BH, grow, n);
           if (s2 != CQS_OK) return s2;
           continue;
         }
-        CK(cudaMemcpyAsync(fb_o[0], hacc_o + grow * BH * D, size_t(n * BH * D * 4),
-                           cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(fb_l[0], hacc_l + grow * BH, size_t(n * BH * 4),
-                           cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(fb_o[b], hacc_o + grow * BH * D, size_t(n * BH * D * 4),
+                           cudaMemcpyHostToDevice, sc.fh));
+        CK(cudaMemcpyAsync(fb_l[b], hacc_l + grow * BH, size_t(n * BH * 4),
+                           cudaMemcpyHostToDevice, sc.fh));
+        CK(cudaEventRecord(fb_loaded[b], sc.fh));
+        CK(cudaStreamWaitEvent(st, fb_loaded[b], 0));
         const float* po = acc_o + lrow * BH * D;
         const float* pl = acc_l + lrow * BH;
-        CK(launch_merge(n, d.B, d.H, d.D, 1, &po, &pl, fb_o[0], fb_l[0], true, nullptr, d.out_dtype,
-                        nullptr, 0, n, nullptr, st));
+        CK(launch_merge(n, d.B, d.H, d.D, 1, &po, &pl, fb_o[b], fb_l[b], true, nullptr,
+                        d.out_dtype, nullptr, 0, n, nullptr, st));
         ++launches;
-        CK(cudaMemcpyAsync(hacc_o + grow * BH * D, fb_o[0], size_t(n * BH * D * 4),
-                           cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(hacc_l + grow * BH, fb_l[0], size_t(n * BH * 4), cudaMemcpyDeviceToHost,
-                           st));
+        CK(cudaEventRecord(fb_merged[b], st));
+        CK(cudaStreamWaitEvent(sc.fd, fb_merged[b], 0));
+        CK(cudaMemcpyAsync(hacc_o + grow * BH * D, fb_o[b], size_t(n * BH * D * 4),
+                           cudaMemcpyDeviceToHost, sc.fd));
+        CK(cudaMemcpyAsync(hacc_l + grow * BH, fb_l[b], size_t(n * BH * 4), cudaMemcpyDeviceToHost,
+                           sc.fd));
+        CK(cudaEventRecord(fb_free[b], sc.fd));
         h2d += uint64_t(n * BH * (D + 1) * 4);
         d2h += uint64_t(n * BH * (D + 1) * 4);
       }
     }
+    if (j > 0) {
+      CK(cudaEventRecord(flush_done, sc.fd));
+      flushed_once = true;
+    }
     gi = ge;
   }
 
-  if (j > 0) {  // host accumulator -> O, lse
+  if (j > 0) {  // host accumulator -> O, lse (after every flush has landed): in = fb 0, out = fb 1
+    CK(cudaEventRecord(flush_done, sc.fd));
+    CK(cudaStreamWaitEvent(sc.fh, flush_done, 0));
     for (int64_t r = 0; r < N; r += F) {
       const int64_t n = std::min(F, N - r);
+      CK(cudaStreamWaitEvent(sc.fh, fb_free[0], 0));   // (never-recorded events are no-ops)
       CK(cudaMemcpyAsync(fb_o[0], hacc_o + r * BH * D, size_t(n * BH * D * 4),
-                         cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(fb_l[0], hacc_l + r * BH, size_t(n * BH * 4), cudaMemcpyHostToDevice, st));
+                         cudaMemcpyHostToDevice, sc.fh));
+      CK(cudaMemcpyAsync(fb_l[0], hacc_l + r * BH, size_t(n * BH * 4), cudaMemcpyHostToDevice, sc.fh));
+      CK(cudaEventRecord(fb_loaded[0], sc.fh));
+      CK(cudaStreamWaitEvent(st, fb_loaded[0], 0));
+      CK(cudaStreamWaitEvent(st, fb_free[1], 0));
       h2d += uint64_t(n * BH * (D + 1) * 4);
-      cqs_status s2 = emit_final(fb_o[0], fb_l[0], r, n);
+      cqs_status s2 = emit_final(1, fb_o[0], fb_l[0], r, n);
       if (s2 != CQS_OK) return s2;
+      CK(cudaEventRecord(fb_free[0], st));   // input consumed by the kernel
     }
   }
+  // the caller's stream must cover every copy issued on the helper streams
+  CK(cudaEventRecord(flush_done, sc.fd));
+  CK(cudaStreamWaitEvent(st, flush_done, 0));
+  CK(cudaEventRecord(flush_done, sc.fh));
+  CK(cudaStreamWaitEvent(st, flush_done, 0));
 
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));

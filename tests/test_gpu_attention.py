@@ -154,3 +154,19 @@ def test_merge_abi_matches_oracle():
     assert np.allclose(got_o, ref_o, atol=1e-5) and np.all(got_o[5] == 0)
     fin = np.isfinite(ref_l)
     assert np.allclose(got_l[fin], ref_l[fin], atol=1e-5) and np.all(np.isneginf(got_l[~fin]))
+
+
+@pytest.mark.parametrize("D", [32, 96, 128])
+def test_f32_head_dims(D):
+    q, k, v = gen(1, 1, 700, D, 41 + D, bf16=False)
+    out, lse = cqs.attention(q, k, v, depth=2)
+    torch.cuda.synchronize()
+    check_f32(out, lse, *ref_dense(q, k, v))
+
+
+def test_bf16_out_f32_depth0_tiny():
+    """N smaller than one tile, single task (depth 0), fp32 output."""
+    q, k, v = gen(1, 3, 37, 64, 17, bf16=True)
+    out, lse = cqs.attention(q, k, v, depth=0, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    check_bf16(out, lse, *ref_dense(q, k, v))

@@ -89,3 +89,12 @@ def test_c3_streamed_16gib_sampled():
         o = out[0, h, rows].double().numpy()
         assert np.abs(o - Oref).max() <= 2e-2
         assert np.abs(lse[0, h, rows].double().numpy() - lref).max() <= 1e-3
+
+
+def test_streamed_batch2_f32_out():
+    q, k, v = host_qkv(2, 2, 1500, 128, 77, torch.bfloat16)
+    d = cqs.make_desc(N=1500, B=2, H=2, D=128, depth=-1, in_dtype="bf16", qkv_loc="host")
+    budget, _ = cqs.cqs_memory_model(d, 2, 1, 1)
+    out, lse, info, st, peak = run_streamed(q, k, v, budget, depth=2, out_dtype="f32")
+    assert info.depth == 2 and peak <= budget + 512
+    check(out, lse, q, k, v, 2e-2, 1e-3)
