@@ -18,6 +18,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "attn_common.cuh"
 #include "ptx.cuh"
 
@@ -287,81 +289,103 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
           for (int c = 0; c < kBN; ++c)
             if (c >= valid) s[c] = -INFINITY;
         }
-        // row max: 8 independent chains (3-input FMNMX3 each step), then a small tree
-        float mx8[8];
+        // One exp2 pass: p = 2^(s*scale_log2 - m_use) fused per 32-column chunk with the packed
+        // row sum, the bf16 pack and the tcgen05.st of P (sums / packs / stores fill the issue
+        // slots between MUFU ops).  With TRACK it also takes the row max of the raw scores on the
+        // side (4 FMNMX3 chains on the ALU pipe) — the "speculative max" of step j > 0 below.
+        auto exp_pass = [&](float m_use, auto track, float& rmax) -> float {
+          constexpr bool kTrack = decltype(track)::value;
+          const uint64_t sc2 = ptx::f2(scale_log2, scale_log2), nm2 = ptx::f2(-m_use, -m_use);
+          uint64_t rs2[4] = {0, 0, 0, 0};
+          float mx4[4];
+          if (kTrack) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) mx8[u] = s[u];
-#pragma unroll
-        for (int c = 8; c < kBN; c += 16) {
-#pragma unroll
-          for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], fmaxf(s[c + u], s[c + 8 + u]));
-        }
-        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
-        const float m_new = (j == 0 || mx > m + kRescaleThreshold) ? mx : m;
-        const bool need = (j > 0) && (m_new != m);
-        if (__any_sync(0xffffffffu, need)) {
-          ptx::mbar_wait(&o_bar[t], (j - 1) & 1);
-          ptx::tc_fence_after();
-          const float f = need ? ptx::ex2(m - m_new) : 1.f;
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            ptx::tmem_ld32(tO + c * 32, ov);
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * f);
-            ptx::tmem_st32(tO + c * 32, ov);
+            for (int u = 0; u < 4; ++u) mx4[u] = -INFINITY;
           }
-          ptx::tmem_st_wait();
-          l *= f;
-        }
-        m = m_new;
-        // Optional MUFU ping-pong between the two softmax warpgroups (named barriers 1 and 2,
-        // -DCQS_PINGPONG): forces the exp2 phases of tile 0 and tile 1 to alternate.  Measured
-        // slower (1071 vs 1107 TFLOP/s on C2): the per-tile S->P time is ~1.9k cycles against a
-        // 1k-cycle MMA chain, so strict alternation only adds waiting; off by default.
-        DBG_T0(tp_max);
-#ifdef CQS_PINGPONG
-        if (two && !(t == 0 && j == 0)) ptx::named_bar_sync(1 + t, 256);
-#endif
-        DBG_T0(tp_gate);
-        const uint64_t sc2 = ptx::f2(scale_log2, scale_log2), nm2 = ptx::f2(-m, -m);
-        // fused per 32-column chunk: exp2 -> packed row-sum -> bf16 pack -> tcgen05.st, so the
-        // sums, packs and TMEM stores fill the issue slots between MUFU ops
-        uint64_t rs2[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int c = 0; c < kBN / 32; ++c) {
-          uint32_t pk[16];
+          for (int c = 0; c < kBN / 32; ++c) {
+            uint32_t pk[16];
 #pragma unroll
-          for (int ii = 0; ii < 16; ++ii) {
-            const int i = 16 * c + ii;
-            float x0, x1;
-            ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
-            if ((kPolyMask >> (i & 7)) & 1) {
-              ptx::exp2_poly_pair(x0, x1);
-              if (2 * i >= valid) x0 = 0.f;   // masked tail columns (poly gives 2^-125)
-              if (2 * i + 1 >= valid) x1 = 0.f;
-            } else {
-              x0 = ptx::ex2(x0);
-              x1 = ptx::ex2(x1);
+            for (int ii = 0; ii < 16; ++ii) {
+              const int i = 16 * c + ii;
+              if (kTrack && (ii & 1) == 0)
+                mx4[(i >> 1) & 3] = fmaxf(mx4[(i >> 1) & 3],
+                                          fmaxf(fmaxf(s[2 * i], s[2 * i + 1]),
+                                                fmaxf(s[2 * i + 2], s[2 * i + 3])));
+              float x0, x1;
+              ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
+              if ((kPolyMask >> (i & 7)) & 1) {
+                ptx::exp2_poly_pair(x0, x1);
+                if (2 * i >= valid) x0 = 0.f;   // masked tail columns (poly gives 2^-125)
+                if (2 * i + 1 >= valid) x1 = 0.f;
+              } else {
+                x0 = ptx::ex2(x0);
+                x1 = ptx::ex2(x1);
+              }
+              rs2[ii & 3] = ptx::fadd2(rs2[ii & 3], ptx::f2(x0, x1));
+              pk[ii] = ptx::pack_bf16(x0, x1);
             }
-            const uint64_t p2 = ptx::f2(x0, x1);
-            rs2[ii & 3] = ptx::fadd2(rs2[ii & 3], p2);
-            pk[ii] = ptx::pack_bf16(x0, x1);
+            ptx::tmem_st16(tS + c * 16, pk);
           }
-          ptx::tmem_st16(tS + c * 16, pk);
-        }
-        DBG_T0(tp_exp);
-#ifdef CQS_PINGPONG
-        if (two && !(t == 1 && j == n_kv - 1)) ptx::named_bar_arrive(2 - t, 256);
-#endif
-        {
+          if (kTrack) rmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
           const uint64_t rr = ptx::fadd2(ptx::fadd2(rs2[0], rs2[1]), ptx::fadd2(rs2[2], rs2[3]));
           float a0, a1;
           ptx::f2_split(rr, a0, a1);
-          l += a0 + a1;
+          return a0 + a1;
+        };
+        float rowsum = 0.f, rmax = 0.f;
+#ifdef CQS_DBG_TIMING
+        long long tp_max = 0, tp_gate = 0, tp_exp = 0;
+#define DBG_MARK(v) v = clock64()
+#else
+#define DBG_MARK(v)
+#endif
+        bool exact_pass = true;   // run the plain pass against the final m
+        if (j == 0) {
+          // first tile: exact row max first (8 FMNMX3 chains, then a small tree)
+          float mx8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) mx8[u] = s[u];
+#pragma unroll
+          for (int c = 8; c < kBN; c += 16) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], fmaxf(s[c + u], s[c + 8 + u]));
+          }
+          m = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                    fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
+        } else {
+          // speculative max: exponentiate against the running max m right away and take this
+          // tile's max on the side; only if it exceeds m by more than the rescale threshold
+          // (2^8; rare after the first tiles) are O and l rescaled and the pass redone.
+          DBG_MARK(tp_max);
+          rowsum = exp_pass(m, std::true_type{}, rmax);
+          const float mx = rmax * scale_log2;
+          const bool need = mx > m + kRescaleThreshold;
+          exact_pass = __any_sync(0xffffffffu, need);
+          if (exact_pass) {
+            const float m_new = need ? mx : m;
+            ptx::tmem_st_wait();
+            ptx::mbar_wait(&o_bar[t], (j - 1) & 1);   // O must hold PV_{j-1}
+            ptx::tc_fence_after();
+            const float f = need ? ptx::ex2(m - m_new) : 1.f;
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t ov[32];
+              ptx::tmem_ld32(tO + c * 32, ov);
+              ptx::tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * f);
+              ptx::tmem_st32(tO + c * 32, ov);
+            }
+            ptx::tmem_st_wait();
+            l *= f;
+            m = m_new;
+          }
         }
+        DBG_MARK(tp_gate);
+        if (exact_pass) rowsum = exp_pass(m, std::false_type{}, rmax);
+        DBG_MARK(tp_exp);
+        l += rowsum;
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
