@@ -21,6 +21,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "ptx.cuh"
 #include "attn_common.cuh"
 #include "task_params.cuh"
@@ -264,81 +266,94 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           for (int c = 0; c < kBN; ++c)
             if (c >= valid) s[c] = -INFINITY;
         }
-        // row max: 8 independent chains (3-input FMNMX3 each step), then a small tree
-        float mx8[8];
+        // One exp2 pass: p = 2^(s*scale_log2 - m_use) (packed FFMA2 argument, MUFU.EX2 — or the
+        // FMA-pipe polynomial for the pairs in kPolyMask), fused per 32-column chunk with the
+        // packed row sum, the bf16 pack and the tcgen05.st of P.  With TRACK it also takes the
+        // row max of the raw scores on the side (speculative max, see below).
+        auto exp_pass = [&](float m_use, auto track, float& rmax) -> float {
+          constexpr bool kTrack = decltype(track)::value;
+          const uint64_t sc2 = ptx::f2(scale_log2, scale_log2), nm2 = ptx::f2(-m_use, -m_use);
+          uint64_t rs2[4] = {0, 0, 0, 0};
+          float mx4[4];
+          if (kTrack) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) mx8[u] = s[u];
-#pragma unroll
-        for (int c = 8; c < kBN; c += 16) {
-#pragma unroll
-          for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], fmaxf(s[c + u], s[c + 8 + u]));
-        }
-        float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
-        const float m_new = (j == 0 || mx > m + kRescaleThreshold) ? mx : m;
-        const bool need = (j > 0) && (m_new != m);
-        if (__any_sync(0xffffffffu, need)) {
-          // O must hold PV_{j-1} before it is rescaled (o_bar phase j-1)
-          ptx::mbar_wait(&o_bar[t], (j - 1) & 1);
-          ptx::tc_fence_after();
-          const float f = need ? ptx::ex2(m - m_new) : 1.f;
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t ov[32];
-            ptx::tmem_ld32(tO + c * 32, ov);
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * f);
-            ptx::tmem_st32(tO + c * 32, ov);
+            for (int u = 0; u < 4; ++u) mx4[u] = -INFINITY;
           }
-          ptx::tmem_st_wait();
-          l *= f;
-        }
-        m = m_new;
-        // MUFU ping-pong between the two softmax warpgroups (named barriers 1, 2; see the
-        // CTA-pair kernel)
-#ifdef CQS_PINGPONG
-        if (two && !(t == 0 && j == 0)) ptx::named_bar_sync(1 + t, 256);
-#endif
-        // p = 2^(s*scale_log2 - m): packed FFMA2 for the argument, MUFU.EX2 for most column pairs
-        // and the FMA-pipe polynomial for the pairs in kPolyMask; fused per 32-column chunk with
-        // the packed row sum, the bf16 pack and the tcgen05.st of P
-        const uint64_t sc2 = ptx::f2(scale_log2, scale_log2), nm2 = ptx::f2(-m, -m);
-        uint64_t rs2[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int c = 0; c < kBN / 32; ++c) {
-          uint32_t pk[16];
+          for (int c = 0; c < kBN / 32; ++c) {
+            uint32_t pk[16];
 #pragma unroll
-          for (int ii = 0; ii < 16; ++ii) {
-            const int i = 16 * c + ii;
-            float x0, x1;
-            ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
-#ifdef CQS_DBG_SKIP_EXP
-            if (true) {
-            } else
-#endif
-            if ((kPolyMask<D> >> (i & 7)) & 1) {
-              ptx::exp2_poly_pair(x0, x1);
-              if (2 * i >= valid) x0 = 0.f;         // masked tail columns (poly gives 2^-125)
-              if (2 * i + 1 >= valid) x1 = 0.f;
-            } else {
-              x0 = ptx::ex2(x0);
-              x1 = ptx::ex2(x1);
+            for (int ii = 0; ii < 16; ++ii) {
+              const int i = 16 * c + ii;
+              if (kTrack && (ii & 1) == 0)
+                mx4[(i >> 1) & 3] = fmaxf(mx4[(i >> 1) & 3],
+                                          fmaxf(fmaxf(s[2 * i], s[2 * i + 1]),
+                                                fmaxf(s[2 * i + 2], s[2 * i + 3])));
+              float x0, x1;
+              ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
+              if ((kPolyMask<D> >> (i & 7)) & 1) {
+                ptx::exp2_poly_pair(x0, x1);
+                if (2 * i >= valid) x0 = 0.f;         // masked tail columns (poly gives 2^-125)
+                if (2 * i + 1 >= valid) x1 = 0.f;
+              } else {
+                x0 = ptx::ex2(x0);
+                x1 = ptx::ex2(x1);
+              }
+              rs2[ii & 3] = ptx::fadd2(rs2[ii & 3], ptx::f2(x0, x1));
+              pk[ii] = ptx::pack_bf16(x0, x1);
             }
-            rs2[ii & 3] = ptx::fadd2(rs2[ii & 3], ptx::f2(x0, x1));
-            pk[ii] = ptx::pack_bf16(x0, x1);
+            ptx::tmem_st16(tS + c * 16, pk);
           }
-          ptx::tmem_st16(tS + c * 16, pk);
-        }
-#ifdef CQS_PINGPONG
-        if (two && !(t == 1 && j == n_kv - 1)) ptx::named_bar_arrive(2 - t, 256);
-#endif
-        {
-          const uint64_t r = ptx::fadd2(ptx::fadd2(rs2[0], rs2[1]), ptx::fadd2(rs2[2], rs2[3]));
+          if (kTrack) rmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+          const uint64_t rr = ptx::fadd2(ptx::fadd2(rs2[0], rs2[1]), ptx::fadd2(rs2[2], rs2[3]));
           float a0, a1;
-          ptx::f2_split(r, a0, a1);
-          l += a0 + a1;
+          ptx::f2_split(rr, a0, a1);
+          return a0 + a1;
+        };
+        float rowsum = 0.f, rmax = 0.f;
+        bool exact_pass = true;
+        if (j == 0) {
+          // first tile: exact row max first (8 FMNMX3 chains, then a small tree)
+          float mx8[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) mx8[u] = s[u];
+#pragma unroll
+          for (int c = 8; c < kBN; c += 16) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], fmaxf(s[c + u], s[c + 8 + u]));
+          }
+          m = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                    fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
+        } else {
+          // speculative max: exponentiate against the running max right away and take this
+          // tile's max on the side; only when it exceeds m by more than the threshold (rare after
+          // the first tiles) are O and l rescaled (O must hold PV_{j-1}) and the pass redone
+          rowsum = exp_pass(m, std::true_type{}, rmax);
+          const float mx = rmax * scale_log2;
+          const bool need = mx > m + kRescaleThreshold;
+          exact_pass = __any_sync(0xffffffffu, need);
+          if (exact_pass) {
+            const float m_new = need ? mx : m;
+            ptx::tmem_st_wait();
+            ptx::mbar_wait(&o_bar[t], (j - 1) & 1);
+            ptx::tc_fence_after();
+            const float f = need ? ptx::ex2(m - m_new) : 1.f;
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+              uint32_t ov[32];
+              ptx::tmem_ld32(tO + c * 32, ov);
+              ptx::tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * f);
+              ptx::tmem_st32(tO + c * 32, ov);
+            }
+            ptx::tmem_st_wait();
+            l *= f;
+            m = m_new;
+          }
         }
+        if (exact_pass) rowsum = exp_pass(m, std::false_type{}, rmax);
+        l += rowsum;
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();

@@ -170,3 +170,17 @@ def test_bf16_out_f32_depth0_tiny():
     out, lse = cqs.attention(q, k, v, depth=0, out_dtype=torch.float32)
     torch.cuda.synchronize()
     check_bf16(out, lse, *ref_dense(q, k, v))
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_bf16_growing_logits_speculative_max(D):
+    """Key norms grow along the sequence, so later key tiles raise the row max by more than the
+    rescale threshold: exercises the speculative-max redo path (O rescale + second exp pass)."""
+    N = 3000
+    q, k, v = gen(1, 2, N, D, 123 + D, bf16=True)
+    ramp = torch.linspace(0.5, 4.0, N, device=DEV).view(1, 1, N, 1)
+    k = (k.float() * ramp).to(torch.bfloat16)
+    for depth in (0, 1, 2):
+        out, lse = cqs.attention(q, k, v, depth=depth)
+        torch.cuda.synchronize()
+        check_bf16(out, lse, *ref_dense(q, k, v))
