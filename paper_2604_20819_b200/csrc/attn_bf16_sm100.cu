@@ -396,14 +396,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 template <int D>
 static cudaError_t launch_bf16_impl(const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
                                     float* acc_lse, float scale, cudaStream_t stream) {
-  static bool configured = false;
+  static std::atomic<uint64_t> configured{0};
   auto kern = attn_bf16_sm100_kernel<D>;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         AttnCfg<D>::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = set_smem_attr_once(kern, AttnCfg<D>::kSmemBytes, configured);
+  if (e != cudaSuccess) return e;
   const int64_t grid = int64_t(tp.n_items) * tp.BH;
   if (grid <= 0) return cudaSuccess;
   kern<<<dim3(unsigned(grid)), kAttnThreads, AttnCfg<D>::kSmemBytes, stream>>>(

@@ -449,14 +449,9 @@ extern "C" int cqs_dbg_reset() {
 
 cudaError_t launch_attn_bf16_pair(const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
                                   float* acc_lse, float scale, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bf16_sm100_2cta_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         pair::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};
+  cudaError_t e = set_smem_attr_once(attn_bf16_sm100_2cta_kernel, pair::kSmemBytes, configured);
+  if (e != cudaSuccess) return e;
   const int64_t grid = 2 * int64_t(tp.n_items) * tp.BH;
   if (grid <= 0) return cudaSuccess;
   attn_bf16_sm100_2cta_kernel<<<dim3(unsigned(grid)), pair::kThreads, pair::kSmemBytes, stream>>>(

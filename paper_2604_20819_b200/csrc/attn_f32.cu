@@ -116,13 +116,9 @@ static cudaError_t launch_f32_impl(int64_t grid, const TaskParams& tp, const flo
                                    const float* k, const float* v, const int64_t* strides,
                                    float* acc_o, float* acc_lse, float scale, cudaStream_t stream) {
   constexpr int smem = (kF32Rows * D + kF32Keys * (D + 1) + kF32Keys * D) * 4;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_f32_kernel<D>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> configured{0};
+  cudaError_t e = set_smem_attr_once(attn_f32_kernel<D>, smem, configured);
+  if (e != cudaSuccess) return e;
   attn_f32_kernel<D><<<dim3(unsigned(grid)), kF32Threads, smem, stream>>>(
       tp, q, k, v, strides[0], strides[1], strides[2], acc_o, acc_lse, scale);
   return cudaGetLastError();

@@ -140,6 +140,9 @@ static bool is_difference_set(const std::vector<int32_t>& I, int c) {
   return true;
 }
 
+// Plan tables hold every task (~200 B each): cap the tree at 7^8 = 5.8M leaves.
+constexpr int64_t kMaxTasks = 5764801;
+
 static int64_t ipow(int64_t b, int e) {
   int64_t r = 1;
   while (e-- > 0) r *= b;
@@ -252,6 +255,8 @@ static cqs_status validate_desc(const cqs_plan_desc* d, std::vector<int32_t>& I)
   if (d->depth < -1 || d->depth >= CQS_MAX_DEPTH) return fail(CQS_E_INVALID, "bad depth");
   if (d->depth >= 0 && d->N < ipow(d->c, d->depth))
     return fail(CQS_E_INVALID, "N < c^depth (R10)");
+  if (d->depth >= 0 && ipow(d->c, d->depth) > kMaxTasks)
+    return fail(CQS_E_UNSUPPORTED, "more than 7^8 tasks: the plan table would not fit host memory");
   if (d->in_dtype == CQS_BF16 && !(d->D == 64 || d->D == 128))
     return fail(CQS_E_UNSUPPORTED, "bf16 path supports D in {64, 128}");
   if (d->in_dtype == CQS_F32 && !(d->D % 32 == 0 && d->D <= 128))
@@ -293,7 +298,9 @@ cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
   const uint64_t budget = d.budget_bytes;
 
   int max_depth = 0;
-  while (max_depth + 1 < CQS_MAX_DEPTH && ipow(d.c, max_depth + 1) <= d.N) ++max_depth;
+  while (max_depth + 1 < CQS_MAX_DEPTH && ipow(d.c, max_depth + 1) <= d.N &&
+         ipow(d.c, max_depth + 1) <= kMaxTasks)
+    ++max_depth;
   const int k_lo = d.depth >= 0 ? d.depth : 0, k_hi = d.depth >= 0 ? d.depth : max_depth;
 
   LeafSet ls;

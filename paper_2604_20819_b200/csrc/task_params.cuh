@@ -1,6 +1,9 @@
 // Per-task launch descriptor shared by the attention kernels (passed by value as a kernel param),
 // and the fused LSE-merge epilogue helpers.
 #pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
 #include <cstdint>
 
 #include "../../include/cqs.h"
@@ -58,6 +61,19 @@ __device__ __forceinline__ void merge_chunk(float* __restrict__ acc, const float
     }
     dst[i] = r;
   }
+}
+
+// Dynamic-smem opt-in is a per-device function attribute: set it once per (kernel, device).
+template <class Kernel>
+inline cudaError_t set_smem_attr_once(Kernel kern, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
 }
 
 }  // namespace cqs
