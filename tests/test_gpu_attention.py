@@ -184,3 +184,14 @@ def test_bf16_growing_logits_speculative_max(D):
         out, lse = cqs.attention(q, k, v, depth=depth)
         torch.cuda.synchronize()
         check_bf16(out, lse, *ref_dense(q, k, v))
+
+
+@pytest.mark.parametrize("c,I,N,depth", [(13, (0, 1, 3, 9), 2000, 1), (13, (0, 1, 3, 9), 3000, 2),
+                                         (7, (0, 1, 5), 2500, 2), (21, (0, 1, 4, 14, 16), 3000, 1)])
+def test_bf16_other_interest_sets(c, I, N, depth):
+    """NEXT-3: the same kernels run CQS Divide with c=13 / 21 and the paired c=7 set (P:350,
+    P:366-368); the decomposition must still reproduce full attention."""
+    q, k, v = gen(1, 2, N, 128, 300 + c + N, bf16=True)
+    out, lse = cqs.attention(q, k, v, depth=depth, offsets=I)
+    torch.cuda.synchronize()
+    check_bf16(out, lse, *ref_dense(q, k, v))

@@ -79,3 +79,13 @@ def test_plan_deterministic():
     a = cqs.cqs_plan_serialize(_plan(1030, 3))
     b = cqs.cqs_plan_serialize(_plan(1030, 3))
     assert a == b
+
+
+@pytest.mark.parametrize("c,I,N,itr", [(13, (0, 1, 3, 9), 400, 2), (21, (0, 1, 4, 14, 16), 500, 1),
+                                       (13, (0, 1, 5, 11), 300, 1)])
+def test_plan_bytes_other_interest_sets(c, I, N, itr):
+    """NEXT-3: larger cyclic difference sets (Appendix B table, and the
+    paired set of (0,1,3,9)) plan bit-exactly like c=7."""
+    p = cqs.cqs_plan(N=N, B=1, H=1, D=64, depth=itr, in_dtype="f32", c=c, offsets=I)
+    assert cqs.cqs_plan_serialize(p) == O.plan_bytes(N, c, I, itr)
+    assert p.info().total_work_pairs == N * N
