@@ -15,10 +15,12 @@ Parts:
   O3  literal Algorithm 1 (raw exp, Num/Den) ...... P:41-52
   O4  LSE form: per-task (O_i, lse_i) + LSE merge . P:240 (Den_i = exp(lse), Num_i = out*Den_i)
   O5  device-memory model (memory_model.py) ....... P:145-162 budget-driven uniform depth (R14)
+  O6  backward: dense gradients + literal Alg. 2 .. P:87-128, Appendix D P:429-502 (NEXT-1)
 
 Pins (tests/test_oracle_*.py, `-m "not gpu"`): Eq. 1 / Fig. 2 / Fig. 3 facts, brute-force pair
 coverage, closed forms (N=1 -> O=V, Q=K=0 -> mean V), an independent pure-Python loop evaluation,
-torch float64 SDPA, granularity invariance and negative controls.  No function here is "parity
+torch float64 SDPA, granularity invariance and negative controls; O6 against central finite
+differences and dO = 0 / linearity-in-V cases.  No function here is "parity
 unpinned".
 """
 from __future__ import annotations
@@ -398,3 +400,61 @@ def cqsa_forward_lse(q, k, v, entries, alpha=None):
     for n in range(N):
         O[:, :, n], lse[:, :, n] = lse_merge(parts[n])
     return O, lse
+
+
+# ------------------------------------------------------------------------------------------------
+# O6. Backward: dense gradients and literal Algorithm 2
+# ------------------------------------------------------------------------------------------------
+
+def dense_attention_grads(q, k, v, dO, alpha=None):
+    """Gradients of L = sum(dO * O), O = softmax(alpha Q K^T) V, per (b, h) plane, float64:
+    dV = P^T dO;  dP = dO V^T;  dS = P * (dP - rowsum(dO * O));  dQ = alpha dS K;  dK = alpha dS^T Q.
+    (The standard softmax chain rule; it is the Num/Den derivation of Appendix D collapsed with
+    O = Num / Den, P:445-465.)"""
+    q, k, v, dO = (np.asarray(t, np.float64) for t in (q, k, v, dO))
+    D = q.shape[-1]
+    alpha = 1.0 / math.sqrt(D) if alpha is None else alpha
+    R = alpha * np.einsum("bhnd,bhmd->bhnm", q, k)
+    P = np.exp(R - R.max(axis=-1, keepdims=True))
+    P /= P.sum(axis=-1, keepdims=True)
+    O = np.einsum("bhnm,bhmd->bhnd", P, v)
+    dV = np.einsum("bhnm,bhnd->bhmd", P, dO)
+    dP = np.einsum("bhnd,bhmd->bhnm", dO, v)
+    delta = (dO * O).sum(axis=-1, keepdims=True)
+    dS = P * (dP - delta)
+    return alpha * np.einsum("bhnm,bhmd->bhnd", dS, k), alpha * np.einsum("bhnm,bhnd->bhmd", dS, q), dV
+
+
+def cqsa_backward_alg2(q, k, v, dO, entries, alpha=None):
+    """Algorithm 2 literally in float64, with Num / Den from Algorithm 1 (raw exp, R7):
+    dNum = dO / Den; dDen = -rowsum(dO * Num) / Den^2 (Eq. 4); per task
+    dV_i = P_i^T dNum_i; dP_i = dNum_i V_i^T + dDen_i 1^T; dR_i = dP_i * P_i; dQ_i = alpha dR_i K_i;
+    dK_i = alpha dR_i^T Q_i (P:117-121, Eq. 5; dK uses Q_i, reading R18 for the P:484 typo);
+    IndexAdd into dQ, dK, dV (Eq. 6)."""
+    q, k, v, dO = (np.asarray(t, np.float64) for t in (q, k, v, dO))
+    B, H, N, D = q.shape
+    alpha = 1.0 / math.sqrt(D) if alpha is None else alpha
+    Num = np.zeros((B, H, N, D))
+    Den = np.zeros((B, H, N))
+    Ps = []
+    for e in entries:                                              # forward (Alg. 1, P:64-74)
+        idx = e.token_ids
+        Pi = np.exp(alpha * np.einsum("bhld,bhmd->bhlm", q[:, :, idx], k[:, :, idx])) * local_mask(e)
+        Ps.append(Pi)
+        np.add.at(Num, (slice(None), slice(None), idx), np.einsum("bhlm,bhmd->bhld", Pi, v[:, :, idx]))
+        np.add.at(Den, (slice(None), slice(None), idx), Pi.sum(axis=-1))
+    dQ, dK, dV = np.zeros_like(q), np.zeros_like(k), np.zeros_like(v)   # P:111
+    dNum = dO / Den[..., None]                                     # P:112
+    dDen = -(dO * Num).sum(axis=-1) / (Den * Den)                  # P:113
+    for e, Pi in zip(entries, Ps):                                 # P:114
+        idx = e.token_ids                                          # P:115
+        dNum_i, dDen_i = dNum[:, :, idx], dDen[:, :, idx]          # P:116
+        dV_i = np.einsum("bhlm,bhld->bhmd", Pi, dNum_i)            # P:117
+        dP_i = np.einsum("bhld,bhmd->bhlm", dNum_i, v[:, :, idx]) + dDen_i[..., None]   # P:118
+        dR_i = dP_i * Pi                                           # P:119
+        dQ_i = alpha * np.einsum("bhlm,bhmd->bhld", dR_i, k[:, :, idx])                # P:120
+        dK_i = alpha * np.einsum("bhlm,bhld->bhmd", dR_i, q[:, :, idx])                # P:121
+        np.add.at(dQ, (slice(None), slice(None), idx), dQ_i)      # P:122
+        np.add.at(dK, (slice(None), slice(None), idx), dK_i)      # P:123
+        np.add.at(dV, (slice(None), slice(None), idx), dV_i)      # P:124
+    return dQ, dK, dV
