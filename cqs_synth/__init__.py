@@ -8,7 +8,7 @@ Recipe (SURVEY.md §8d "Synthetic inputs"):
   h_j   = splitmix64_finalize(K0 * (4*seed + tid) + K1 * (3*e + j))   for j = 0, 1, 2   (mod 2^64)
   u_0..u_11 = the four 16-bit lanes of h_0, h_1, h_2
   x     = (sum_i u_i - 6 * 2^16) / 2^16          (Irwin-Hall(12): mean ~0, variance ~1, |x| <= 6)
-where e is the row-major flat index over [B, H, N, D] and tid is 0 for Q, 1 for K, 2 for V.
+where e is the row-major flat index over [B, H, N, D] and tid is 0 for Q, 1 for K, 2 for V, 3 for dO.
 The integer sum is exact in fp32; bf16 inputs are the fp32 value rounded to nearest-even.
 
 Two implementations with bit-identical results: `numpy_*` (uint64, well defined wrap-around) and
@@ -22,7 +22,7 @@ K0 = 0x9E3779B97F4A7C15
 K1 = 0xD1B54A32D192ED03
 M1 = 0xBF58476D1CE4E5B9
 M2 = 0x94D049BB133111EB
-TID = {"q": 0, "k": 1, "v": 2}
+TID = {"q": 0, "k": 1, "v": 2, "do": 3}   # "do": the upstream gradient dO of the backward
 BASE_SEED = 20260417  # seed = 20260417 + config index
 
 

@@ -159,6 +159,41 @@ cqs_status cqs_attention_forward(const cqs_plan_t* plan, const void* q, const vo
  * acc_o [N][B*H][D], acc_lse [N][B*H] (natural log; -inf = no contribution yet). */
 cqs_status cqs_partial_view(const cqs_plan_t* plan, void* dev_ws, float** acc_o, float** acc_lse);
 
+/* ---------------------------------------------------------------------------------------------
+ * Backward (Algorithm 2; gradient derivation Appendix D).
+ *
+ * The paper's backward re-gathers each task's Q/K/V/O/dO/lse, runs an FA backward on
+ * the leaf with the GLOBAL lse and Delta = rowsum(dO * O) (so per-leaf probabilities are the global
+ * P), and IndexAdds dQ/dK/dV.  Here each task runs two tcgen05 kernels that
+ * read the tensors in place through TMA and accumulate into fp32 dQ/dK/dV workspaces:
+ *   P = exp(alpha q.k - lse_q),  dP = dO V^T,  dS = P (dP - Delta_q)        on every kept block
+ *   dV += P^T dO,  dK += alpha dS^T Q  (one CTA per 128-key tile, loops over the query tiles of the
+ *   query segments that keep its key segment);   dQ += alpha dS K  (one CTA per 128-query tile).
+ * Resident bf16 plans only (desc.qkv_loc = device, in_dtype = bf16, world = 1); the plan is the
+ * forward's plan (same depth, same tasks).  Sum over tasks = the dense attention gradient (R19).
+ * --------------------------------------------------------------------------------------------- */
+/* Device workspace of cqs_attention_backward: Delta/lse [B*H][2][round_up(N,4)] fp32 and three fp32
+ * accumulators [N][B*H][D] (dQ, dK, dV), each section 256-byte aligned.  CQS_E_UNSUPPORTED for a
+ * plan the backward does not run (see above). */
+cqs_status cqs_backward_workspace_size(const cqs_plan_t* plan, size_t* dev_bytes);
+
+/* Gradients of L = sum(dO * O) for the forward O = attention(q, k, v) of this plan.
+ *   q, k, v, o, dout : device bf16 [B,H,N,D] with element strides qkv_strides (all five tensors
+ *                      share the layout; stride D = 1; 16-byte aligned rows, for TMA).
+ *   lse              : device fp32 [B,H,N] contiguous, the forward's natural-log lse.
+ *   dq, dk, dv       : device [B,H,N,D] of desc.out_dtype with element strides grad_strides
+ *                      (stride D = 1); fully overwritten.
+ *   scale            : alpha (<= 0 selects 1/sqrt(D)); must equal the forward's.
+ *   dev_ws           : >= cqs_backward_workspace_size() bytes, 256-byte aligned, caller-owned.
+ * Asynchronous on `stream` unless stats != NULL (ms_attn = task kernels, ms_merge = prep + cast).
+ * Errors: CQS_E_INVALID (NULL / misaligned / bad strides), CQS_E_UNSUPPORTED (plan kind),
+ * CQS_E_CUDA (launch failure; cqs_last_error has the CUDA message). */
+cqs_status cqs_attention_backward(const cqs_plan_t* plan, const void* q, const void* k,
+                                  const void* v, const void* o, const void* dout,
+                                  const int64_t qkv_strides[4], const float* lse, void* dq,
+                                  void* dk, void* dv, const int64_t grad_strides[4], float scale,
+                                  void* dev_ws, void* stream /* cudaStream_t */, cqs_stats* stats);
+
 /* Rows owned by `rank` for the final merge: [row0, row0 + rows) with row0 = floor(rank N / world). */
 cqs_status cqs_shard_rows(int64_t N, int32_t world, int32_t rank, int64_t* row0, int64_t* rows);
 

@@ -458,3 +458,21 @@ def cqsa_backward_alg2(q, k, v, dO, entries, alpha=None):
         np.add.at(dK, (slice(None), slice(None), idx), dK_i)
         np.add.at(dV, (slice(None), slice(None), idx), dV_i)
     return dQ, dK, dV
+
+
+def dense_dq_rows(q, k, v, dO, rows, alpha=None, block=1 << 16):
+    """dQ for query `rows` of one [N, D] plane (the dQ of dense_attention_grads row by row, for
+    sizes where the full N x N matrices do not fit): O_r and lse_r from dense_attention_rows, then
+    dQ_r = alpha sum_j P_rj (dO_r . v_j - dO_r . O_r) k_j with keys streamed in blocks."""
+    N, D = k.shape
+    alpha = 1.0 / math.sqrt(D) if alpha is None else alpha
+    Or, lse = dense_attention_rows(q, k, v, rows, alpha, block)
+    qr = np.asarray(q[rows], np.float64)
+    dOr = np.asarray(dO[rows], np.float64)
+    delta = (dOr * Or).sum(axis=1)
+    dq = np.zeros((len(rows), D))
+    for s in range(0, N, block):
+        kb = np.asarray(k[s:s + block], np.float64); vb = np.asarray(v[s:s + block], np.float64)
+        P = np.exp(alpha * qr @ kb.T - lse[:, None])
+        dq += (P * (dOr @ vb.T - delta[:, None])) @ kb
+    return alpha * dq

@@ -6,8 +6,9 @@ no fallback: if libcqs.so is missing the import of the library raises immediatel
 
 Same names as the C ABI: cqs_plan, cqs_plan_info, cqs_plan_task, cqs_plan_serialize,
 cqs_memory_model, cqs_forward_workspace_size, cqs_attention_forward, cqs_partial_view,
-cqs_shard_rows, cqs_merge.  `attention()` is a convenience wrapper (allocates the workspace with
-torch and calls the above).
+cqs_shard_rows, cqs_merge, cqs_backward_workspace_size, cqs_attention_backward.  `attention()` and
+`attention_backward()` are convenience wrappers (allocate the workspace with torch and call the
+above).
 """
 from __future__ import annotations
 
@@ -30,7 +31,7 @@ ABI_SYMBOLS = ("cqs_plan", "cqs_plan_info", "cqs_plan_task", "cqs_plan_serialize
                "cqs_plan_destroy", "cqs_memory_model", "cqs_forward_workspace_size",
                "cqs_attention_forward", "cqs_partial_view", "cqs_shard_rows", "cqs_merge",
                "cqs_ipc_handle", "cqs_ipc_open", "cqs_ipc_close", "cqs_last_error",
-               "cqs_abi_version")
+               "cqs_abi_version", "cqs_backward_workspace_size", "cqs_attention_backward")
 
 
 class CqsError(RuntimeError):
@@ -102,6 +103,10 @@ def lib():
         L.cqs_merge.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                 C.POINTER(P), C.POINTER(P), P, P, P, C.c_int,
                                 C.POINTER(C.c_int64), C.c_int64, C.c_int64, P, P]
+        L.cqs_backward_workspace_size.argtypes = [P, C.POINTER(C.c_size_t)]
+        L.cqs_attention_backward.argtypes = [P, P, P, P, P, P, C.POINTER(C.c_int64), P, P, P, P,
+                                             C.POINTER(C.c_int64), C.c_float, P, P,
+                                             C.POINTER(Stats)]
         L.cqs_ipc_handle.argtypes = [P, P, C.POINTER(C.c_uint64)]
         L.cqs_ipc_open.argtypes = [P, C.POINTER(P)]
         L.cqs_ipc_close.argtypes = [P]
@@ -229,6 +234,30 @@ def cqs_attention_forward(plan: Plan, q, k, v, out, lse=None, scale=0.0, budget_
     return st
 
 
+def cqs_backward_workspace_size(plan: Plan) -> int:
+    dv = C.c_size_t()
+    _check(lib().cqs_backward_workspace_size(plan.handle, C.byref(dv)))
+    return dv.value
+
+
+def cqs_attention_backward(plan: Plan, q, k, v, o, dout, lse, dq, dk, dv, scale=0.0, dev_ws=None,
+                           stream=None, stats=False):
+    """q/k/v/o/dout: bf16 device tensors [B,H,N,D] sharing one layout (stride(D)=1); lse: fp32
+    [B,H,N] contiguous (the forward's); dq/dk/dv: [B,H,N,D] of the plan's out dtype, one layout."""
+    for t in (k, v, o, dout):
+        if tuple(t.stride()) != tuple(q.stride()):
+            raise ValueError("q, k, v, o, dout must share one layout")
+    for t in (dk, dv):
+        if tuple(t.stride()) != tuple(dq.stride()):
+            raise ValueError("dq, dk, dv must share one layout")
+    st = Stats() if stats else None
+    _check(lib().cqs_attention_backward(
+        plan.handle, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _i64x4(q.stride()), _ptr(lse),
+        _ptr(dq), _ptr(dk), _ptr(dv), _i64x4(dq.stride()), float(scale), _ptr(dev_ws),
+        _stream_ptr(stream), C.byref(st) if st is not None else None))
+    return st
+
+
 def cqs_partial_view(plan: Plan, dev_ws):
     o, l_ = C.c_void_p(), C.c_void_p()
     _check(lib().cqs_partial_view(plan.handle, _ptr(dev_ws), C.byref(o), C.byref(l_)))
@@ -295,3 +324,19 @@ def attention(q, k, v, depth=1, budget_bytes=0, out_dtype=None, scale=0.0, want_
     lse = torch.empty((B, H, N), dtype=torch.float32, device=q.device) if want_lse else None
     st = cqs_attention_forward(p, q, k, v, out, lse, scale, budget_bytes, ws, None, stats=stats)
     return (out, lse, st) if stats else (out, lse)
+
+
+def attention_backward(q, k, v, o, dout, lse, depth=1, scale=0.0, grad_dtype=None,
+                       offsets=(0, 1, 3), stats=False):
+    """Gradients (dq, dk, dv) of sum(dout * o) for o = attention(q, k, v) (bf16 device tensors
+    [B,H,N,D]; lse the forward's fp32 [B,H,N]) through Algorithm 2 at CQS depth `depth`."""
+    import torch
+    B, H, N, D = q.shape
+    gdt = grad_dtype or q.dtype
+    p = cqs_plan(N=N, B=B, H=H, D=D, depth=depth, in_dtype=CQS_BF16,
+                 out_dtype=CQS_BF16 if gdt == torch.bfloat16 else CQS_F32, offsets=offsets,
+                 c=len(offsets) * (len(offsets) - 1) + 1)
+    ws = torch.empty(max(cqs_backward_workspace_size(p), 256), dtype=torch.uint8, device=q.device)
+    dq, dk, dv = (torch.empty((B, H, N, D), dtype=gdt, device=q.device) for _ in range(3))
+    st = cqs_attention_backward(p, q, k, v, o, dout, lse, dq, dk, dv, scale, ws, stats=stats)
+    return (dq, dk, dv, st) if stats else (dq, dk, dv)

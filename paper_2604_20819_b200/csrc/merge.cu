@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Finalize (no parts): O = acc_o (0 where acc_lse = -inf), lse = acc_lse; a pure streaming
+// Finalize (no parts): O = acc_o (0 where acc_lse = -inf; acc_lse may be NULL), lse = acc_lse; a pure streaming
 // copy + cast.  Thread -> (unit, float4 column) with D4 = D/4 a power of two (shift), 32-bit index
 // math when the unit count fits (the 64-bit divisions of a flat int64 index ran on the XU pipe
 // and held this kernel at 62% of the HBM roofline).
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(256)
       const Idx f = b + u * stride;
       if (f < n4) {
         v[u] = reinterpret_cast<const float4*>(acc_o)[f];
-        l[u] = acc_lse[f >> d4_shift];
+        l[u] = acc_lse ? acc_lse[f >> d4_shift] : 0.f;   // NULL: plain cast (backward)
       }
     }
 #pragma unroll

@@ -59,3 +59,15 @@ def test_alg2_negative_control():
     ref = O.dense_attention_grads(q, k, v, dO)
     got = O.cqsa_backward_alg2(q, k, v, dO, ents)
     assert max(np.max(np.abs(g - r)) for g, r in zip(got, ref)) > 1e-3
+
+
+def test_dense_dq_rows_matches_full_gradient():
+    """The row-streamed dQ (used for sampled rows at full size) equals dense_attention_grads' dQ,
+    itself pinned to finite differences above; small blocks force several key blocks."""
+    rng = np.random.default_rng(12)
+    N, D = 300, 16
+    q, k, v, dO = (rng.standard_normal((1, 1, N, D)) for _ in range(4))
+    dQ, _, _ = O.dense_attention_grads(q, k, v, dO)
+    rows = np.array([0, 7, 150, 299])
+    got = O.dense_dq_rows(q[0, 0], k[0, 0], v[0, 0], dO[0, 0], rows, block=64)
+    assert np.abs(got - dQ[0, 0, rows]).max() < 1e-12
