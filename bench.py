@@ -180,6 +180,8 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-bwd", action="store_true",
+                    help="skip the backward (Algorithm 2, SURVEY NEXT-1) measurement")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N>1: merge over peer memory in one kernel (p2p) or NCCL all-to-all + merge")
     args = ap.parse_args()
@@ -277,6 +279,56 @@ def main():
         dist.all_reduce(launches_t)
         launches = int(launches_t.item())
 
+    # ---- backward (Algorithm 2, NEXT-1): dQ/dK/dV of sum(dO*O) for this step's O / lse, resident,
+    #      world = 1; its own line item, not part of the forward `value` ----
+    bwd = None
+    if not args.no_bwd and bf and D in (64, 128):
+        do = cqs_synth.torch_tensor((B, H, N, D), SEED, "do", torch.bfloat16, dev)
+        if world > 1:   # O / lse of every row on every rank (untimed setup: the forward's output)
+            bo, bl = cqs.attention(q, k, v, depth=depth)
+        else:
+            bo, bl = out, lse
+        bws = torch.empty(cqs.cqs_backward_workspace_size(p0), dtype=torch.uint8, device=dev)
+        dq, dk, dv = (torch.empty_like(q) for _ in range(3))
+        pgr = cdist.PeerGradReduce(p0, bws, N, B, H, D, world, rank) if world > 1 else None
+
+        def bstep(with_stats):
+            st = cqs.cqs_attention_backward(p0, q, k, v, bo, do, bl, dq, dk, dv, 0.0, bws,
+                                            stream, stats=with_stats)
+            if pgr is not None:   # owner sums the ranks' partial rows over peer memory
+                pgr.reduce(dq, dk, dv, stream)
+            return st
+
+        bstep(False)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        n_b = max(1, min(args.steps, 3))
+        b_attn = 0.0
+        with ClockSampler(local) as bclk:
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(n_b):
+                b_attn += bstep(True).ms_attn
+            g1.record(stream)
+            torch.cuda.synchronize()
+        b_ms = g0.elapsed_time(g1) / n_b
+        if world > 1:
+            t = torch.tensor([b_ms], device=dev if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            b_ms = float(t.item())
+            pgr.close()
+        bflops = 10.0 * N * N * D * BH
+        my_frac = info.my_work_pairs / info.total_work_pairs
+        bwd = {"metric": "exact-attn backward TFLOP/s (algorithmic 10*N^2*D*B*H)",
+               "value": bflops / (b_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": b_ms,
+               "steps": n_b,
+               "kernel_tflops_executed": 1.4 * bflops * my_frac / (b_attn / n_b * 1e-3) / 1e12,
+               "ratio_to_forward_time": b_ms / ms, "clocks": bclk.summary(),
+               "path": "cqs_attention_backward: prep + per task bwd_dkdv + bwd_dq (tcgen05) + casts"
+                       + (" ; PeerGradReduce sum over NVLink" if world > 1 else "")}
+        del bws, dq, dk, dv, do
+
     # ---- end-to-end through the public C-ABI call with HOST buffers (streamed mode: per-task H2D
     #      of the needed segments double-buffered against compute, O / lse D2H) ----
     e2e = None
@@ -357,6 +409,7 @@ def main():
                      "note": "all device bytes live during the timed steps (Q/K/V/O/lse + "
                              "workspace; torch caching-allocator view, no budget set for C2)"},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+        "backward": bwd,
     }
     print(json.dumps(line))
     if world > 1:

@@ -1,6 +1,6 @@
 /*
  * cqs.h — C ABI of libcqs: exact softmax attention decomposed by CQS Divide (Stream-CQSA,
- * arXiv 2604.20819), B200 (sm_100a) forward hot path.
+ * arXiv 2604.20819), B200 (sm_100a): forward hot path, backward (Algorithm 2), multi-GPU exchange.
  *
  * Citations: P:n = PAPER.md line n (section in brackets).  R<n> = DESIGN.md reading n.
  *
@@ -169,8 +169,12 @@ cqs_status cqs_partial_view(const cqs_plan_t* plan, void* dev_ws, float** acc_o,
  *   P = exp(alpha q.k - lse_q),  dP = dO V^T,  dS = P (dP - Delta_q)        on every kept block
  *   dV += P^T dO,  dK += alpha dS^T Q  (one CTA per 128-key tile, loops over the query tiles of the
  *   query segments that keep its key segment);   dQ += alpha dS K  (one CTA per 128-query tile).
- * Resident bf16 plans only (desc.qkv_loc = device, in_dtype = bf16, world = 1); the plan is the
- * forward's plan (same depth, same tasks).  Sum over tasks = the dense attention gradient (R19).
+ * Resident bf16 plans only (desc.qkv_loc = device, in_dtype = bf16); the plan has the forward's
+ * depth and tasks.  Sum over tasks = the dense attention gradient (R19).  With world > 1 each rank
+ * runs ITS tasks (LPT, as in the forward) into full-size fp32 partial accumulators that stay in
+ * dev_ws (cqs_backward_partial_view); the row owner then sums the ranks' partial rows with
+ * cqs_reduce_sum (over peer memory or after an all-to-all) — one exchange, no communication
+ * during compute.
  * --------------------------------------------------------------------------------------------- */
 /* Device workspace of cqs_attention_backward: Delta/lse [B*H][2][round_up(N,4)] fp32 and three fp32
  * accumulators [N][B*H][D] (dQ, dK, dV), each section 256-byte aligned.  CQS_E_UNSUPPORTED for a
@@ -182,7 +186,7 @@ cqs_status cqs_backward_workspace_size(const cqs_plan_t* plan, size_t* dev_bytes
  *                      share the layout; stride D = 1; 16-byte aligned rows, for TMA).
  *   lse              : device fp32 [B,H,N] contiguous, the forward's natural-log lse.
  *   dq, dk, dv       : device [B,H,N,D] of desc.out_dtype with element strides grad_strides
- *                      (stride D = 1); fully overwritten.
+ *                      (stride D = 1); fully overwritten.  Ignored (may be NULL) when world > 1.
  *   scale            : alpha (<= 0 selects 1/sqrt(D)); must equal the forward's.
  *   dev_ws           : >= cqs_backward_workspace_size() bytes, 256-byte aligned, caller-owned.
  * Asynchronous on `stream` unless stats != NULL (ms_attn = task kernels, ms_merge = prep + cast).
@@ -193,6 +197,20 @@ cqs_status cqs_attention_backward(const cqs_plan_t* plan, const void* q, const v
                                   const int64_t qkv_strides[4], const float* lse, void* dq,
                                   void* dk, void* dv, const int64_t grad_strides[4], float scale,
                                   void* dev_ws, void* stream /* cudaStream_t */, cqs_stats* stats);
+
+/* Pointers to the fp32 gradient accumulators inside dev_ws after cqs_attention_backward:
+ * dQ, dK, dV, each [N][B*H][D] (token-major, so a row shard is one contiguous block). */
+cqs_status cqs_backward_partial_view(const cqs_plan_t* plan, void* dev_ws, float** dq, float** dk,
+                                     float** dv);
+
+/* R-way sum (Alg. 2's IndexAdd across ranks), on device: for r < rows, p < B*H,
+ *   out[b, h, out_row0 + r, :] = cast_out_dtype( sum_j parts[j][r][p][:] )
+ * parts: HOST array of n_parts (1..16) device pointers to [rows][B*H][D] fp32 (16-byte aligned;
+ * peer pointers from cqs_ipc_open allowed); out: [B,H,N,D] with element strides out_strides
+ * (stride D = 1).  D must be a power of two in [4, 256].  Errors: CQS_E_INVALID. */
+cqs_status cqs_reduce_sum(int64_t rows, int32_t B, int32_t H, int32_t D, int32_t n_parts,
+                          const float* const* parts, void* out, cqs_dtype out_dtype,
+                          const int64_t out_strides[4], int64_t out_row0, void* stream);
 
 /* Rows owned by `rank` for the final merge: [row0, row0 + rows) with row0 = floor(rank N / world). */
 cqs_status cqs_shard_rows(int64_t N, int32_t world, int32_t rank, int64_t* row0, int64_t* rows);

@@ -425,12 +425,14 @@ def dense_attention_grads(q, k, v, dO, alpha=None):
     return alpha * np.einsum("bhnm,bhmd->bhnd", dS, k), alpha * np.einsum("bhnm,bhnd->bhmd", dS, q), dV
 
 
-def cqsa_backward_alg2(q, k, v, dO, entries, alpha=None):
+def cqsa_backward_alg2(q, k, v, dO, entries, alpha=None, only=None):
     """Algorithm 2 literally in float64, with Num / Den from Algorithm 1 (raw exp, R7):
     dNum = dO / Den; dDen = -rowsum(dO * Num) / Den^2 (Eq. 4); per task
     dV_i = P_i^T dNum_i; dP_i = dNum_i V_i^T + dDen_i 1^T; dR_i = dP_i * P_i; dQ_i = alpha dR_i K_i;
     dK_i = alpha dR_i^T Q_i (P:117-121, Eq. 5; dK uses Q_i, reading R18 for the P:484 typo);
-    IndexAdd into dQ, dK, dV (Eq. 6)."""
+    IndexAdd into dQ, dK, dV (Eq. 6).  `only` (optional set of task indices) restricts
+    the loop of P:114 to those tasks — one rank's share of a task-sharded backward; the forward
+    quantities Num / Den still come from all tasks."""
     q, k, v, dO = (np.asarray(t, np.float64) for t in (q, k, v, dO))
     B, H, N, D = q.shape
     alpha = 1.0 / math.sqrt(D) if alpha is None else alpha
@@ -446,7 +448,9 @@ def cqsa_backward_alg2(q, k, v, dO, entries, alpha=None):
     dQ, dK, dV = np.zeros_like(q), np.zeros_like(k), np.zeros_like(v)
     dNum = dO / Den[..., None]
     dDen = -(dO * Num).sum(axis=-1) / (Den * Den)
-    for e, Pi in zip(entries, Ps):
+    for t, (e, Pi) in enumerate(zip(entries, Ps)):
+        if only is not None and t not in only:
+            continue
         idx = e.token_ids
         dNum_i, dDen_i = dNum[:, :, idx], dDen[:, :, idx]
         dV_i = np.einsum("bhlm,bhld->bhmd", Pi, dNum_i)

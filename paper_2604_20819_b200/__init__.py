@@ -6,7 +6,8 @@ no fallback: if libcqs.so is missing the import of the library raises immediatel
 
 Same names as the C ABI: cqs_plan, cqs_plan_info, cqs_plan_task, cqs_plan_serialize,
 cqs_memory_model, cqs_forward_workspace_size, cqs_attention_forward, cqs_partial_view,
-cqs_shard_rows, cqs_merge, cqs_backward_workspace_size, cqs_attention_backward.  `attention()` and
+cqs_shard_rows, cqs_merge, cqs_backward_workspace_size, cqs_attention_backward,
+cqs_backward_partial_view, cqs_reduce_sum.  `attention()` and
 `attention_backward()` are convenience wrappers (allocate the workspace with torch and call the
 above).
 """
@@ -31,7 +32,8 @@ ABI_SYMBOLS = ("cqs_plan", "cqs_plan_info", "cqs_plan_task", "cqs_plan_serialize
                "cqs_plan_destroy", "cqs_memory_model", "cqs_forward_workspace_size",
                "cqs_attention_forward", "cqs_partial_view", "cqs_shard_rows", "cqs_merge",
                "cqs_ipc_handle", "cqs_ipc_open", "cqs_ipc_close", "cqs_last_error",
-               "cqs_abi_version", "cqs_backward_workspace_size", "cqs_attention_backward")
+               "cqs_abi_version", "cqs_backward_workspace_size", "cqs_attention_backward",
+               "cqs_backward_partial_view", "cqs_reduce_sum")
 
 
 class CqsError(RuntimeError):
@@ -107,6 +109,9 @@ def lib():
         L.cqs_attention_backward.argtypes = [P, P, P, P, P, P, C.POINTER(C.c_int64), P, P, P, P,
                                              C.POINTER(C.c_int64), C.c_float, P, P,
                                              C.POINTER(Stats)]
+        L.cqs_backward_partial_view.argtypes = [P, P, C.POINTER(P), C.POINTER(P), C.POINTER(P)]
+        L.cqs_reduce_sum.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                     C.POINTER(P), P, C.c_int, C.POINTER(C.c_int64), C.c_int64, P]
         L.cqs_ipc_handle.argtypes = [P, P, C.POINTER(C.c_uint64)]
         L.cqs_ipc_open.argtypes = [P, C.POINTER(P)]
         L.cqs_ipc_close.argtypes = [P]
@@ -248,14 +253,33 @@ def cqs_attention_backward(plan: Plan, q, k, v, o, dout, lse, dq, dk, dv, scale=
         if tuple(t.stride()) != tuple(q.stride()):
             raise ValueError("q, k, v, o, dout must share one layout")
     for t in (dk, dv):
-        if tuple(t.stride()) != tuple(dq.stride()):
+        if dq is not None and tuple(t.stride()) != tuple(dq.stride()):
             raise ValueError("dq, dk, dv must share one layout")
     st = Stats() if stats else None
     _check(lib().cqs_attention_backward(
         plan.handle, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _i64x4(q.stride()), _ptr(lse),
-        _ptr(dq), _ptr(dk), _ptr(dv), _i64x4(dq.stride()), float(scale), _ptr(dev_ws),
-        _stream_ptr(stream), C.byref(st) if st is not None else None))
+        _ptr(dq), _ptr(dk), _ptr(dv), _i64x4(dq.stride()) if dq is not None else None,
+        float(scale), _ptr(dev_ws), _stream_ptr(stream), C.byref(st) if st is not None else None))
     return st
+
+
+def cqs_backward_partial_view(plan: Plan, dev_ws):
+    """Device addresses of the fp32 dQ, dK, dV accumulators ([N][B*H][D]) inside dev_ws."""
+    a, b, c = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    _check(lib().cqs_backward_partial_view(plan.handle, _ptr(dev_ws), C.byref(a), C.byref(b),
+                                           C.byref(c)))
+    return a.value, b.value, c.value
+
+
+def cqs_reduce_sum(rows, B, H, D, parts, out, out_row0=0, stream=None):
+    """out[:, :, out_row0:out_row0+rows] = sum of the fp32 parts ([rows, B*H, D] device tensors
+    or raw device addresses, e.g. peer memory), cast to out's dtype."""
+    import torch
+    n = len(parts)
+    pp = (C.c_void_p * max(n, 1))(*[_addr(t) for t in parts])
+    od = CQS_BF16 if out.dtype == torch.bfloat16 else CQS_F32
+    _check(lib().cqs_reduce_sum(int(rows), B, H, D, n, pp, _ptr(out), od, _i64x4(out.stride()),
+                                int(out_row0), _stream_ptr(stream)))
 
 
 def cqs_partial_view(plan: Plan, dev_ws):

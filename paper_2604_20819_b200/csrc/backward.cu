@@ -52,8 +52,8 @@ static BwdLayout bwd_layout(const cqs_plan_desc& d) {
 static cqs_status bwd_supported(const cqs_plan_t* p) {
   if (!p) return fail(CQS_E_INVALID, "plan is NULL");
   const cqs_plan_desc& d = p->desc;
-  if (d.qkv_loc != CQS_LOC_DEVICE || d.in_dtype != CQS_BF16 || d.world != 1)
-    return fail(CQS_E_UNSUPPORTED, "backward runs resident bf16 plans with world = 1");
+  if (d.qkv_loc != CQS_LOC_DEVICE || d.in_dtype != CQS_BF16)
+    return fail(CQS_E_UNSUPPORTED, "backward runs resident bf16 plans");
   if (d.D != 64 && d.D != 128) return fail(CQS_E_UNSUPPORTED, "backward head dim must be 64 or 128");
   if (int64_t(d.N) * d.B * d.H >= (int64_t(1) << 31))
     return fail(CQS_E_UNSUPPORTED, "backward: N*B*H must stay below 2^31");
@@ -72,6 +72,19 @@ extern "C" cqs_status cqs_backward_workspace_size(const cqs_plan_t* p, size_t* d
   return CQS_OK;
 }
 
+extern "C" cqs_status cqs_backward_partial_view(const cqs_plan_t* p, void* dev_ws, float** dq,
+                                                float** dk, float** dv) {
+  if (!dev_ws || !dq || !dk || !dv) return fail(CQS_E_INVALID, "NULL argument");
+  cqs_status s = bwd_supported(p);
+  if (s != CQS_OK) return s;
+  const BwdLayout L = bwd_layout(p->desc);
+  uint8_t* ws = static_cast<uint8_t*>(dev_ws);
+  *dq = reinterpret_cast<float*>(ws + L.dq);
+  *dk = reinterpret_cast<float*>(ws + L.dk);
+  *dv = reinterpret_cast<float*>(ws + L.dv);
+  return CQS_OK;
+}
+
 extern "C" cqs_status cqs_attention_backward(const cqs_plan_t* p, const void* q, const void* k,
                                              const void* v, const void* o, const void* dout,
                                              const int64_t qkv_strides[4], const float* lse,
@@ -81,9 +94,10 @@ extern "C" cqs_status cqs_attention_backward(const cqs_plan_t* p, const void* q,
   cqs_status s = bwd_supported(p);
   if (s != CQS_OK) return s;
   const cqs_plan_desc& d = p->desc;
-  if (!q || !k || !v || !o || !dout || !lse || !dq || !dk || !dv || !dev_ws)
+  const bool cast = d.world == 1;   // world > 1: partial accumulators stay in dev_ws
+  if (!q || !k || !v || !o || !dout || !lse || !dev_ws || (cast && (!dq || !dk || !dv)))
     return fail(CQS_E_INVALID, "NULL argument");
-  if (!qkv_strides || qkv_strides[3] != 1 || !grad_strides || grad_strides[3] != 1)
+  if (!qkv_strides || qkv_strides[3] != 1 || (cast && (!grad_strides || grad_strides[3] != 1)))
     return fail(CQS_E_INVALID, "strides: stride(D) must be 1");
   if (reinterpret_cast<uintptr_t>(dev_ws) & 255) return fail(CQS_E_INVALID, "dev_ws must be 256B aligned");
   if ((reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(dout)) & 15)
@@ -146,11 +160,11 @@ extern "C" cqs_status cqs_attention_backward(const cqs_plan_t* p, const void* q,
   mark();
   float* accs[3] = {acc_dq, acc_dk, acc_dv};
   void* outs[3] = {dq, dk, dv};
-  for (int i = 0; i < 3 && e == cudaSuccess; ++i)
+  for (int i = 0; i < 3 && e == cudaSuccess && cast; ++i)
     e = launch_merge(d.N, d.B, d.H, d.D, 0, nullptr, nullptr, accs[i], nullptr, false, outs[i],
                      d.out_dtype, grad_strides, 0, d.N, nullptr, st);
   mark();
-  launches += 3;
+  launches += cast ? 3 : 0;
   if (e != cudaSuccess) return fail(CQS_E_CUDA, std::string("backward cast: ") + cudaGetErrorString(e));
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));

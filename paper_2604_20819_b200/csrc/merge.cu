@@ -244,3 +244,74 @@ extern "C" cqs_status cqs_merge(int64_t rows, int32_t B, int32_t H, int32_t D, i
   if (e != cudaSuccess) return fail(CQS_E_CUDA, std::string("cqs_merge: ") + cudaGetErrorString(e));
   return CQS_OK;
 }
+
+// ---------------------------------------------------------------------------------------------
+// R-way SUM of fp32 partial gradients (multi-GPU backward, Alg. 2's IndexAdd across ranks,
+// P:122-124): out[b,h,row0+r,:] = cast(sum_j part_j[r][p][:]).  Thread -> (unit, float4 column),
+// all R loads in flight before the adds; parts may be peer (NVLink) pointers.
+// ---------------------------------------------------------------------------------------------
+namespace cqs {
+
+template <typename OutT>
+__global__ void __launch_bounds__(256)
+    reduce_sum_kernel(int64_t nunits, int BH, int H, int d4_shift, MergeParts parts,
+                      OutT* __restrict__ out, int64_t sB, int64_t sH, int64_t sN,
+                      int64_t out_row0) {
+  const int64_t n4 = nunits << d4_shift;
+  for (int64_t f = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; f < n4;
+       f += int64_t(gridDim.x) * blockDim.x) {
+    float4 v[kMaxMergeParts];
+#pragma unroll
+    for (int j = 0; j < kMaxMergeParts; ++j)
+      if (j < parts.n) v[j] = reinterpret_cast<const float4*>(parts.o[j])[f];
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < kMaxMergeParts; ++j)
+      if (j < parts.n) s.x += v[j].x, s.y += v[j].y, s.z += v[j].z, s.w += v[j].w;
+    const int64_t unit = f >> d4_shift;
+    const int d = int(f & ((int64_t(1) << d4_shift) - 1)) * 4;
+    const int64_t r = unit / BH;
+    const int p = int(unit - r * BH);
+    const int bb = p / H, hh = p - bb * H;
+    store4(out + int64_t(bb) * sB + int64_t(hh) * sH + (out_row0 + r) * sN + d, s);
+  }
+}
+
+}  // namespace cqs
+
+extern "C" cqs_status cqs_reduce_sum(int64_t rows, int32_t B, int32_t H, int32_t D,
+                                     int32_t n_parts, const float* const* parts, void* out,
+                                     cqs_dtype out_dtype, const int64_t out_strides[4],
+                                     int64_t out_row0, void* stream) {
+  using namespace cqs;
+  if (rows < 0 || B < 1 || H < 1 || D < 4 || D > 256 || (D & (D - 1)) != 0 || n_parts < 1 ||
+      n_parts > kMaxMergeParts)
+    return fail(CQS_E_INVALID, "cqs_reduce_sum: bad sizes (D a power of two in [4,256], 1..16 parts)");
+  if (!parts || !out || !out_strides || out_strides[3] != 1 || out_row0 < 0)
+    return fail(CQS_E_INVALID, "cqs_reduce_sum: NULL parts/out or stride(D) != 1");
+  MergeParts mp{};
+  mp.n = n_parts;
+  for (int j = 0; j < n_parts; ++j) {
+    if (!parts[j] || (reinterpret_cast<uintptr_t>(parts[j]) & 15))
+      return fail(CQS_E_INVALID, "cqs_reduce_sum: NULL or non-16-byte-aligned part");
+    mp.o[j] = parts[j];
+  }
+  const int64_t nunits = rows * int64_t(B) * H;
+  if (nunits == 0) return CQS_OK;
+  int shift = 0;
+  while ((4 << shift) < D) ++shift;
+  const int64_t n4 = nunits * (D / 4);
+  const int64_t blocks = std::min<int64_t>((n4 + 255) / 256, 148 * 32);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (out_dtype == CQS_BF16)
+    reduce_sum_kernel<__nv_bfloat16><<<unsigned(blocks), 256, 0, st>>>(
+        nunits, B * H, H, shift, mp, static_cast<__nv_bfloat16*>(out), out_strides[0],
+        out_strides[1], out_strides[2], out_row0);
+  else
+    reduce_sum_kernel<float><<<unsigned(blocks), 256, 0, st>>>(
+        nunits, B * H, H, shift, mp, static_cast<float*>(out), out_strides[0], out_strides[1],
+        out_strides[2], out_row0);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(CQS_E_CUDA, std::string("cqs_reduce_sum: ") + cudaGetErrorString(e));
+  return CQS_OK;
+}

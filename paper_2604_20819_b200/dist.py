@@ -12,8 +12,8 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import cqs_ipc_close, cqs_ipc_handle, cqs_ipc_open, cqs_merge, cqs_partial_view, \
-    cqs_shard_rows
+from . import cqs_backward_partial_view, cqs_ipc_close, cqs_ipc_handle, cqs_ipc_open, cqs_merge, \
+    cqs_partial_view, cqs_reduce_sum, cqs_shard_rows
 
 
 def shard_spans(N: int, world: int):
@@ -93,6 +93,76 @@ class PeerExchange:
         dist.barrier(group=self.group)
         cqs_merge(self.rows, self.B, self.H, self.D, self.po, self.pl, out=out, out_row0=self.row0,
                   n_total=self.N, lse_out=lse, stream=stream)
+        torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+        dist.barrier(group=self.group)
+
+    def close(self):
+        for b in self.opened:
+            cqs_ipc_close(b)
+        self.opened = []
+
+
+# ------------------------------------------------------------------------------------------------
+# Backward (Algorithm 2, NEXT-1) across ranks: every rank accumulates the gradients of ITS tasks
+# into full-size fp32 [N][B*H][D] partials (cqs_backward_partial_view); the owner of each row shard
+# sums the ranks' rows (Alg. 2's IndexAdd, done across GPUs) with cqs_reduce_sum.
+# ------------------------------------------------------------------------------------------------
+
+def exchange_rows(acc: torch.Tensor, N: int, world: int, rank: int, group=None):
+    """acc: [N, W] partial of this rank.  Returns ([world*rows, W] rank-major rows of this rank's
+    shard from every rank, row0, rows) — the all-to-all transport (NCCL on GPUs, gloo on CPU)."""
+    spans = shard_spans(N, world)
+    row0, rows = spans[rank]
+    recv = acc.new_empty((world * rows, acc.shape[1]))
+    dist.all_to_all_single(recv, acc.contiguous(), [rows] * world, [n for _, n in spans],
+                           group=group)
+    return recv, row0, rows
+
+
+def reduce_grads_gpu(recv, world, rows, B, H, D, out, row0, stream=None):
+    """Sum the received rank-major partial rows into rows [row0, row0+rows) of `out`."""
+    cqs_reduce_sum(rows, B, H, D, [recv[r * rows:(r + 1) * rows] for r in range(world)], out,
+                   out_row0=row0, stream=stream)
+
+
+class PeerGradReduce:
+    """Backward exchange + sum in one kernel per gradient over peer memory: every rank maps all
+    ranks' dQ/dK/dV partial accumulators (CUDA IPC, handles swapped once) and sums the peers' rows
+    of its shard directly over NVLink / NVSwitch into its dQ/dK/dV.  The backward workspace must
+    stay allocated (same address) for the object's lifetime."""
+
+    def __init__(self, plan, bws, N, B, H, D, world, rank, group=None):
+        self.N, self.B, self.H, self.D, self.world, self.rank = N, B, H, D, world, rank
+        self.group = group
+        views = cqs_backward_partial_view(plan, bws)
+        mine = [cqs_ipc_handle(a) for a in views]
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self.row0, self.rows = cqs_shard_rows(N, world, rank)
+        self.opened = []
+        self.parts = [[], [], []]          # per gradient: one address per rank
+        BH = B * H
+        for r in range(world):
+            bases = {}
+            for g in range(3):
+                if r == rank:
+                    addr = views[g]
+                else:
+                    h, off = allh[r][g]
+                    if h not in bases:
+                        bases[h] = cqs_ipc_open(h)
+                        self.opened.append(bases[h])
+                    addr = bases[h] + off
+                self.parts[g].append(addr + self.row0 * BH * D * 4)
+
+    def reduce(self, dq, dk, dv, stream=None):
+        """After every rank's backward was issued: barrier, three sum kernels reading the peers'
+        rows over NVLink, barrier (peers done reading before the workspace is reused)."""
+        torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+        dist.barrier(group=self.group)
+        for g, out in enumerate((dq, dk, dv)):
+            cqs_reduce_sum(self.rows, self.B, self.H, self.D, self.parts[g], out,
+                           out_row0=self.row0, stream=stream)
         torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
         dist.barrier(group=self.group)
 

@@ -82,3 +82,55 @@ def test_two_rank_exchange_reproduces_dense(N, depth, tmp_path):
         assert np.abs(Om - Od[row0:row0 + rows]).max() < 1e-12
         assert np.abs(lm - ld[row0:row0 + rows]).max() < 1e-12
     assert tot_work == N * N
+
+
+def _bwd_worker(rank, world, port, N, H, D, depth, outdir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import cqs_synth
+    import paper_2604_20819_b200 as cqs
+    from paper_2604_20819_b200 import dist as cdist
+    from oracle import cqs_oracle as O
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    q, k, v, do = (cqs_synth.numpy_tensor((1, H, N, D), 78, n) for n in ("q", "k", "v", "do"))
+    plan = cqs.cqs_plan(N=N, B=1, H=H, D=64, depth=depth, in_dtype="bf16", world=world, rank=rank)
+    info = plan.info()   # (the planner's task sharding does not depend on D; D=16 keeps it small)
+    entries, mine = [], set()
+    for t in range(info.n_tasks):
+        task = plan.task(t)
+        entries.append(O.build_subseq_entry(N, 7, I, tuple(task.quorum[i] for i in range(depth))))
+        if task.rank == rank:
+            mine.add(t)
+    grads = O.cqsa_backward_alg2(q, k, v, do, entries, only=mine)   # this rank's partials
+    out = []
+    for g in grads:   # token-major [N, H*D] like cqs_backward_partial_view
+        acc = torch.from_numpy(np.ascontiguousarray(g[0].transpose(1, 0, 2).reshape(N, H * D)))
+        recv, row0, rows = cdist.exchange_rows(acc, N, world, rank)
+        out.append(sum(recv[r * rows:(r + 1) * rows].numpy() for r in range(world)))
+    np.save(os.path.join(outdir, "g%d.npy" % rank), np.stack(out))
+    np.save(os.path.join(outdir, "s%d.npy" % rank), np.array([row0, rows, len(mine)]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("N,depth", [(343, 2), (500, 1)])
+def test_two_rank_backward_exchange_reproduces_dense_grads(N, depth, tmp_path):
+    """Task-sharded backward: each rank IndexAdds only its LPT tasks' gradients (Alg. 2 loop
+    P:114-124 split across ranks), the owner sums the exchanged rows; the union equals the dense
+    gradients."""
+    import cqs_synth
+    from oracle import cqs_oracle as O
+    world, H, D = 2, 2, 16
+    mp.start_processes(_bwd_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path)),
+                       nprocs=world, start_method="fork")
+    q, k, v, do = (cqs_synth.numpy_tensor((1, H, N, D), 78, n) for n in ("q", "k", "v", "do"))
+    ref = [g[0].transpose(1, 0, 2).reshape(N, H * D) for g in O.dense_attention_grads(q, k, v, do)]
+    ntasks = 0
+    for r in range(world):
+        row0, rows, nt = np.load(tmp_path / ("s%d.npy" % r))
+        ntasks += nt
+        got = np.load(tmp_path / ("g%d.npy" % r))
+        for g, rf in zip(got, ref):
+            assert np.abs(g - rf[row0:row0 + rows]).max() < 1e-10
+    assert ntasks == 7 ** depth
