@@ -210,14 +210,15 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-        cfg["depth"] = max(cfg["depth"], 2)   # 49 tasks: LPT balance across ranks
+        cfg["schedule"] = "hybrid"   # mixed-depth leaves: LPT makespan within 1% (NEXT-2, R20)
     N, B, H, D, depth = cfg["N"], cfg["B"], cfg["H"], cfg["D"], cfg["depth"]
     bf = cfg["dtype"] == "bf16"
     dt = torch.bfloat16 if bf else torch.float32
     q, k, v = cqs_synth.torch_qkv(B, H, N, D, SEED, dtype=dt, device=dev)
     out = torch.empty(B, H, N, D, dtype=dt, device=dev)
     lse = torch.empty(B, H, N, dtype=torch.float32, device=dev)
-    desc_kw = dict(N=N, B=B, H=H, D=D, depth=depth, in_dtype=cfg["dtype"], world=world, rank=rank)
+    desc_kw = dict(N=N, B=B, H=H, D=D, depth=depth, in_dtype=cfg["dtype"], world=world, rank=rank,
+                   schedule=cfg.get("schedule", "uniform"))
     p0 = cqs.cqs_plan(**desc_kw)
     info = p0.info()
     dev_bytes, _ = cqs.cqs_forward_workspace_size(p0)
@@ -389,7 +390,8 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
         "config": {"workload": cfg["desc"], "N": N, "B": B, "H": H, "D": D, "depth": info.depth,
-                   "tasks": info.n_tasks, "l2": "inputs %.1f GB >> 126 MB L2 (no flush needed)"
+                   "max_depth": info.max_depth, "schedule": cfg.get("schedule", "uniform"),
+                   "tasks": info.n_tasks, "my_work_frac": info.my_work_pairs / info.total_work_pairs, "l2": "inputs %.1f GB >> 126 MB L2 (no flush needed)"
                    % (3 * q.numel() * q.element_size() / 1e9),
                    "parallelism": "task-sharded x%d" % world,
                    "exchange": args.exchange if world > 1 else None},

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define CQS_ABI_VERSION 1
+#define CQS_ABI_VERSION 2
 #define CQS_MAX_DEPTH 12   /* N >= 7^depth and N < 2^31 imply depth <= 11 for c = 7           */
 #define CQS_MAX_SEGS 32    /* segments per task; observed <= 8 up to depth 11     */
 
@@ -65,7 +65,16 @@ typedef struct {
   cqs_loc qkv_loc;           /* where Q, K, V live: device (resident) or pinned host (stream) */
   cqs_loc out_loc;           /* where O and lse live                                          */
   int32_t world, rank;       /* task sharding across `world` GPUs; world=1 on 1 GPU */
+  int32_t schedule;          /* CQS_SCHED_UNIFORM: every leaf at `depth`.  CQS_SCHED_HYBRID
+                                (resident plans, P:158 hybrid scheduling): start from the uniform
+                                tree and split the heaviest leaf into its c children until the LPT
+                                makespan over `world` ranks is within 1% of work/world (or 4096
+                                leaves); a no-op for world = 1.  Leaves then sit at mixed depths. */
+  int32_t reserved;          /* 0 */
 } cqs_plan_desc;
+
+#define CQS_SCHED_UNIFORM 0
+#define CQS_SCHED_HYBRID 1
 
 typedef struct cqs_plan_s cqs_plan_t; /* opaque, library-owned, immutable */
 
@@ -73,7 +82,7 @@ typedef struct {
   int32_t depth;                 /* itr actually planned                                       */
   int32_t acc_depth;             /* device accumulator tier: rows of one depth-j subtree (0=all N) */
   int32_t n_stage_buffers;       /* streamed mode: staging buffers (1 or 2), 0 when resident   */
-  int32_t reserved;
+  int32_t max_depth;             /* deepest leaf (= depth for uniform plans)                   */
   int64_t n_tasks;               /* c^depth                                            */
   int64_t n_empty;               /* tasks with no kept pair (never launched, R9)               */
   int64_t max_task_rows;         /* longest leaf                                               */
@@ -89,6 +98,8 @@ typedef struct {
 typedef struct {
   int32_t nseg;                        /* maximal segments of consecutive tokens, constant codes */
   int32_t rank;                        /* owning rank (-1 if empty)                              */
+  int32_t depth;                       /* leaf depth (quorum[0..depth) is its path from the root) */
+  int32_t reserved;
   uint64_t work;                       /* kept (query, key) pairs                                */
   int32_t quorum[CQS_MAX_DEPTH];       /* (q_1..q_depth)                                   */
   int64_t seg_start[CQS_MAX_SEGS];     /* global token id of the segment's first token          */
@@ -111,7 +122,9 @@ cqs_status cqs_plan_info(const cqs_plan_t* plan, cqs_plan_info_t* info);
 cqs_status cqs_plan_task(const cqs_plan_t* plan, int64_t idx, cqs_task_t* task);
 /* Canonical plan bytes (little endian): "CQSP", u32 version=1, i64 N, i32 c, i32 l, i32 I[l],
  * i32 depth, i64 n_tasks, then per task in lexicographic order: i32 nseg, u64 work,
- * nseg x (i64 start, i64 len, u8 codes[depth]), nseg x u32 kept mask.
+ * nseg x (i64 start, i64 len, u8 codes[depth]), nseg x u32 kept mask.  A hybrid plan whose
+ * leaves differ in depth writes version=2: the same, with i32 leaf depth before each task's nseg
+ * and codes[leaf depth] per segment (tasks in DFS order of their quorum paths).
  * If buf is NULL or *len too small, *len receives the required size and CQS_E_INVALID (buf NULL:
  * CQS_OK) is returned. */
 cqs_status cqs_plan_serialize(const cqs_plan_t* plan, void* buf, size_t* len);

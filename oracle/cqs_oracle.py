@@ -16,6 +16,7 @@ Parts:
   O4  LSE form: per-task (O_i, lse_i) + LSE merge . P:240 (Den_i = exp(lse), Num_i = out*Den_i)
   O5  device-memory model (memory_model.py) ....... P:145-162 budget-driven uniform depth (R14)
   O6  backward: dense gradients + literal Alg. 2 .. P:87-128, Appendix D P:429-502 (NEXT-1)
+  O7  hybrid scheduling: leaf rule + plan bytes ..... P:154-160 (NEXT-2, reading R20)
 
 Pins (tests/test_oracle_*.py, `-m "not gpu"`): Eq. 1 / Fig. 2 / Fig. 3 facts, brute-force pair
 coverage, closed forms (N=1 -> O=V, Q=K=0 -> mean V), an independent pure-Python loop evaluation,
@@ -269,6 +270,59 @@ def plan_bytes(N, c, I, itr) -> bytes:
     """Canonical bytes of the whole plan, from the literal Algorithm 3 (small/medium N)."""
     ents = build_subseq(N, c, itr, I)
     return plan_header_bytes(N, c, I, itr, len(ents)) + b"".join(entry_bytes(e) for e in ents)
+
+
+def hybrid_plan_bytes(N, c, I, base_itr, leaves) -> bytes:
+    """Canonical bytes of a hybrid plan (version 2, include/cqs.h): `leaves` = quorum paths of
+    mixed length in DFS order; each leaf is the literal Algorithm 3 subsequence of its path."""
+    b = PLAN_MAGIC + struct.pack("<I", 2)
+    b += struct.pack("<qii", N, c, len(I)) + struct.pack("<%di" % len(I), *I)
+    b += struct.pack("<iq", base_itr, len(leaves))
+    for qt in leaves:
+        b += struct.pack("<i", len(qt)) + entry_bytes(build_subseq_entry(N, c, I, tuple(qt)))
+    return b
+
+
+# ------------------------------------------------------------------------------------------------
+# O7. Hybrid scheduling (P:158: "some subsequences at itr=1 can be further divided ... while others
+#     remain unchanged"), DESIGN reading R20: which leaves to divide is this build's rule — start
+#     from the uniform tree, LPT the leaves over `world` ranks, and while the makespan exceeds
+#     1.01 x total/world divide the heaviest leaf (first in DFS order on ties) into its c children.
+# ------------------------------------------------------------------------------------------------
+
+def leaf_work(N, c, I, qt) -> int:
+    e = build_subseq_entry(N, c, I, tuple(qt))
+    segs = entry_segments(e)
+    return entry_work(segs, segment_kept_matrix(e, segs))
+
+
+def lpt(works, world):
+    """LPT: largest first (stable on index), each to the least-loaded rank (lowest on ties).
+    Returns (ranks, loads)."""
+    order = sorted(range(len(works)), key=lambda i: -works[i])
+    loads = [0] * world
+    ranks = [-1] * len(works)
+    for i in order:
+        if works[i] == 0:
+            continue
+        r = min(range(world), key=lambda x: (loads[x], x))
+        ranks[i] = r
+        loads[r] += works[i]
+    return ranks, loads
+
+
+def hybrid_leaves(N, c, I, base_itr, world, tol=0.01, max_leaves=4096):
+    leaves = [qt for qt in quorum_tuples(c, base_itr)]
+    works = [leaf_work(N, c, I, qt) for qt in leaves]
+    total = sum(works)
+    while True:
+        _, loads = lpt(works, world)
+        if max(loads) <= (1 + tol) * total / world or len(leaves) + c - 1 > max_leaves:
+            return leaves
+        i = max(range(len(leaves)), key=lambda j: (works[j], -j))
+        kids = [tuple(leaves[i]) + (q,) for q in range(c)]
+        leaves[i:i + 1] = kids
+        works[i:i + 1] = [leaf_work(N, c, I, qt) for qt in kids]
 
 
 # ------------------------------------------------------------------------------------------------

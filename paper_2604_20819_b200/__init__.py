@@ -23,6 +23,7 @@ CQS_OK, CQS_E_VERIFY, CQS_E_INFEASIBLE, CQS_E_INVALID, CQS_E_CUDA, CQS_E_NCCL, C
     CQS_E_UNSUPPORTED = range(8)
 CQS_F32, CQS_BF16 = 0, 1
 CQS_LOC_DEVICE, CQS_LOC_PINNED_HOST = 0, 1
+CQS_SCHED_UNIFORM, CQS_SCHED_HYBRID = 0, 1
 CQS_MAX_DEPTH, CQS_MAX_SEGS = 12, 32
 STATUS_NAMES = {0: "CQS_OK", 1: "CQS_E_VERIFY", 2: "CQS_E_INFEASIBLE", 3: "CQS_E_INVALID",
                 4: "CQS_E_CUDA", 5: "CQS_E_NCCL", 6: "CQS_E_OOM", 7: "CQS_E_UNSUPPORTED"}
@@ -47,12 +48,13 @@ class PlanDesc(C.Structure):
                 ("c", C.c_int32), ("l", C.c_int32), ("offsets", C.POINTER(C.c_int32)),
                 ("depth", C.c_int32), ("budget_bytes", C.c_uint64), ("in_dtype", C.c_int),
                 ("out_dtype", C.c_int), ("qkv_loc", C.c_int), ("out_loc", C.c_int),
-                ("world", C.c_int32), ("rank", C.c_int32)]
+                ("world", C.c_int32), ("rank", C.c_int32), ("schedule", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class PlanInfo(C.Structure):
     _fields_ = [("depth", C.c_int32), ("acc_depth", C.c_int32), ("n_stage_buffers", C.c_int32),
-                ("reserved", C.c_int32), ("n_tasks", C.c_int64), ("n_empty", C.c_int64),
+                ("max_depth", C.c_int32), ("n_tasks", C.c_int64), ("n_empty", C.c_int64),
                 ("max_task_rows", C.c_int64), ("max_staged_rows", C.c_int64),
                 ("total_work_pairs", C.c_uint64), ("my_tasks", C.c_int64),
                 ("my_work_pairs", C.c_uint64), ("dev_workspace_bytes", C.c_uint64),
@@ -60,7 +62,8 @@ class PlanInfo(C.Structure):
 
 
 class Task(C.Structure):
-    _fields_ = [("nseg", C.c_int32), ("rank", C.c_int32), ("work", C.c_uint64),
+    _fields_ = [("nseg", C.c_int32), ("rank", C.c_int32), ("depth", C.c_int32),
+                ("reserved", C.c_int32), ("work", C.c_uint64),
                 ("quorum", C.c_int32 * CQS_MAX_DEPTH), ("seg_start", C.c_int64 * CQS_MAX_SEGS),
                 ("seg_len", C.c_int64 * CQS_MAX_SEGS),
                 ("seg_codes", (C.c_uint8 * CQS_MAX_DEPTH) * CQS_MAX_SEGS),
@@ -146,14 +149,17 @@ def _loc_code(x):
 
 
 def make_desc(N, B, H, D, depth=1, budget_bytes=0, in_dtype="bf16", out_dtype=None,
-              qkv_loc="device", out_loc=None, world=1, rank=0, c=7, offsets=(0, 1, 3)):
+              qkv_loc="device", out_loc=None, world=1, rank=0, c=7, offsets=(0, 1, 3),
+              schedule="uniform"):
     offs = (C.c_int32 * len(offsets))(*offsets)
     d = PlanDesc(N=N, B=B, H=H, D=D, c=c, l=len(offsets), offsets=offs, depth=depth,
                  budget_bytes=int(budget_bytes), in_dtype=_dtype_code(in_dtype),
                  out_dtype=_dtype_code(out_dtype if out_dtype is not None else in_dtype),
                  qkv_loc=_loc_code(qkv_loc),
                  out_loc=_loc_code(out_loc if out_loc is not None else qkv_loc),
-                 world=world, rank=rank)
+                 world=world, rank=rank,
+                 schedule={"uniform": CQS_SCHED_UNIFORM, "hybrid": CQS_SCHED_HYBRID}.get(
+                     schedule, schedule))
     d._offs = offs  # keep alive
     return d
 

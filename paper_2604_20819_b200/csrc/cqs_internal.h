@@ -20,6 +20,7 @@ struct Seg {
 struct Task {
   int32_t nseg = 0;
   int32_t rank = -1;
+  int32_t depth = 0;             // leaf depth (uniform plans: the plan depth; hybrid: per leaf)
   uint64_t work = 0;
   int64_t seg_off = 0;           // into cqs_plan::segs
   int32_t quorum[CQS_MAX_DEPTH] = {};
@@ -31,7 +32,8 @@ struct Task {
 struct cqs_plan_s {
   cqs_plan_desc desc;                // offsets pointer re-pointed at I below
   std::vector<int32_t> I;
-  int32_t depth = 0;
+  int32_t depth = 0;                 // base (uniform) depth; hybrid leaves are at depth >= this
+  int32_t max_depth = 0;             // deepest leaf
   int32_t acc_depth = 0;             // streamed mode accumulator tier
   int32_t n_stage_buffers = 0;
   std::vector<cqs::Task> tasks;      // c^depth, lexicographic

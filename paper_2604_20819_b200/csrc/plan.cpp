@@ -179,49 +179,143 @@ struct LeafSet {
   uint64_t total_work = 0;
 };
 
+// One leaf: segments of the subsequence at path quorum[0..depth), its kept segment-pair blocks,
+// exact work and staged rows (segments touched by a kept block).
+static cqs_status make_leaf(const cqs_plan_desc& d, const std::vector<int32_t>& I,
+                            const int32_t* quorum, int depth, Task& T, std::vector<Seg>& segs,
+                            int64_t* rows_out, int64_t* staged_out) {
+  if (!build_segments(d.N, d.c, I, quorum, depth, segs))
+    return fail(CQS_E_UNSUPPORTED, "task has more than CQS_MAX_SEGS segments");
+  T = Task{};
+  T.depth = depth;
+  std::copy(quorum, quorum + depth, T.quorum);
+  T.nseg = int32_t(segs.size());
+  uint32_t used = 0;
+  int64_t rows = 0;
+  for (int a = 0; a < T.nseg; ++a) {
+    rows += segs[a].len;
+    for (int b = 0; b < T.nseg; ++b)
+      if (kept_pair(segs[a], segs[b], depth)) {
+        T.kept[a] |= 1u << b;
+        T.work += uint64_t(segs[a].len) * uint64_t(segs[b].len);
+        used |= (1u << a) | (1u << b);
+      }
+  }
+  int64_t staged = 0;
+  for (int a = 0; a < T.nseg; ++a)
+    if (used & (1u << a)) staged += segs[a].len;
+  *rows_out = rows;
+  *staged_out = staged;
+  return CQS_OK;
+}
+
+static void add_leaf(LeafSet& ls, Task& T, const std::vector<Seg>& segs, int64_t rows,
+                     int64_t staged) {
+  T.seg_off = int64_t(ls.segs.size());
+  ls.segs.insert(ls.segs.end(), segs.begin(), segs.end());
+  ls.total_work += T.work;
+  if (T.work == 0) ls.n_empty++;
+  ls.max_rows = std::max(ls.max_rows, rows);
+  ls.max_staged = std::max(ls.max_staged, staged);
+  ls.tasks.push_back(T);
+}
+
 static cqs_status enumerate_leaves(const cqs_plan_desc& d, const std::vector<int32_t>& I,
                                    int depth, LeafSet& ls) {
   const int c = d.c;
   const int64_t n = ipow(c, depth);
-  ls.tasks.assign(size_t(n), Task{});
-  ls.segs.clear();
-  ls.n_empty = ls.max_rows = ls.max_staged = 0;
-  ls.total_work = 0;
+  ls = LeafSet{};
+  ls.tasks.reserve(size_t(n));
   ls.segs.reserve(size_t(n) * 4);
   std::vector<Seg> segs;
   int32_t qt[CQS_MAX_DEPTH] = {};
+  Task T;
   for (int64_t idx = 0; idx < n; ++idx) {
     int64_t r = idx;                                       // lexicographic, q_1 most significant
     for (int t = depth - 1; t >= 0; --t) {
       qt[t] = int32_t(r % c);
       r /= c;
     }
-    if (!build_segments(d.N, c, I, qt, depth, segs))
-      return fail(CQS_E_UNSUPPORTED, "task has more than CQS_MAX_SEGS segments");
-    Task& T = ls.tasks[size_t(idx)];
-    std::copy(qt, qt + depth, T.quorum);
-    T.nseg = int32_t(segs.size());
-    T.seg_off = int64_t(ls.segs.size());
-    uint32_t used = 0;
-    int64_t rows = 0;
-    for (int a = 0; a < T.nseg; ++a) {
-      rows += segs[a].len;
-      for (int b = 0; b < T.nseg; ++b)
-        if (kept_pair(segs[a], segs[b], depth)) {
-          T.kept[a] |= 1u << b;
-          T.work += uint64_t(segs[a].len) * uint64_t(segs[b].len);
-          used |= (1u << a) | (1u << b);
-        }
-    }
-    int64_t staged = 0;
-    for (int a = 0; a < T.nseg; ++a)
-      if (used & (1u << a)) staged += segs[a].len;
-    ls.segs.insert(ls.segs.end(), segs.begin(), segs.end());
-    ls.total_work += T.work;
-    if (T.work == 0) ls.n_empty++;
-    ls.max_rows = std::max(ls.max_rows, rows);
-    ls.max_staged = std::max(ls.max_staged, staged);
+    int64_t rows, staged;
+    cqs_status st = make_leaf(d, I, qt, depth, T, segs, &rows, &staged);
+    if (st != CQS_OK) return st;
+    add_leaf(ls, T, segs, rows, staged);
   }
+  return CQS_OK;
+}
+
+// LPT on exact work (largest first, ties by index) -> least-loaded rank (ties lowest rank).
+// Writes Task::rank; returns the makespan.
+static uint64_t lpt_assign(std::vector<Task>& tasks, int world) {
+  std::vector<int64_t> order;
+  for (int64_t i = 0; i < int64_t(tasks.size()); ++i) {
+    tasks[size_t(i)].rank = -1;
+    if (tasks[size_t(i)].work > 0) order.push_back(i);
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    return tasks[size_t(a)].work > tasks[size_t(b)].work;
+  });
+  std::vector<uint64_t> load(size_t(world), 0);
+  for (int64_t i : order) {
+    const size_t r = size_t(std::min_element(load.begin(), load.end()) - load.begin());
+    tasks[size_t(i)].rank = int32_t(r);
+    load[r] += tasks[size_t(i)].work;
+  }
+  return *std::max_element(load.begin(), load.end());
+}
+
+// Hybrid scheduling (Fig. "schedule" right): leaves at mixed depths.  Starting from the
+// uniform tree, repeatedly replace the heaviest leaf (ties: first in DFS order) by its c children
+// until the LPT makespan is within 1% of total/world.  Any such tree is still an exact
+// decomposition: a node's c children partition its kept pairs (the per-level invariant of CQS
+// Divide), so every ordered pair stays covered exactly once.
+constexpr int64_t kMaxHybridLeaves = 4096;
+static cqs_status refine_hybrid(const cqs_plan_desc& d, const std::vector<int32_t>& I,
+                                LeafSet& ls) {
+  struct Leaf {
+    Task T;
+    std::vector<Seg> segs;
+    int64_t rows, staged;
+  };
+  std::vector<Leaf> leaves(ls.tasks.size());
+  for (size_t i = 0; i < ls.tasks.size(); ++i) {
+    const Task& T = ls.tasks[i];
+    leaves[i].T = T;
+    leaves[i].segs.assign(ls.segs.begin() + T.seg_off, ls.segs.begin() + T.seg_off + T.nseg);
+    int64_t rows = 0;
+    for (auto& sg : leaves[i].segs) rows += sg.len;
+    leaves[i].rows = rows;
+    leaves[i].staged = rows;
+  }
+  const uint64_t total = ls.total_work;
+  for (;;) {
+    std::vector<Task> ts;
+    for (auto& L : leaves) ts.push_back(L.T);
+    const uint64_t span = lpt_assign(ts, d.world);
+    if (double(span) <= 1.01 * double(total) / d.world) break;
+    if (int64_t(leaves.size()) + d.c - 1 > kMaxHybridLeaves) break;
+    size_t best = 0;
+    for (size_t i = 1; i < leaves.size(); ++i)
+      if (leaves[i].T.work > leaves[best].T.work) best = i;
+    const Task P = leaves[best].T;
+    if (P.depth + 1 >= CQS_MAX_DEPTH) break;
+    // children need at least one token per chunk of the parent's length
+    if (leaves[best].rows < d.c) break;
+    std::vector<Leaf> kids(size_t(d.c));
+    int32_t qt[CQS_MAX_DEPTH] = {};
+    std::copy(P.quorum, P.quorum + P.depth, qt);
+    for (int q = 0; q < d.c; ++q) {
+      qt[P.depth] = q;
+      cqs_status st = make_leaf(d, I, qt, P.depth + 1, kids[size_t(q)].T, kids[size_t(q)].segs,
+                                &kids[size_t(q)].rows, &kids[size_t(q)].staged);
+      if (st != CQS_OK) return st;
+    }
+    leaves.erase(leaves.begin() + long(best));
+    leaves.insert(leaves.begin() + long(best), kids.begin(), kids.end());
+  }
+  LeafSet out;
+  for (auto& L : leaves) add_leaf(out, L.T, L.segs, L.rows, L.staged);
+  ls = std::move(out);
   return CQS_OK;
 }
 
@@ -263,6 +357,11 @@ static cqs_status validate_desc(const cqs_plan_desc* d, std::vector<int32_t>& I)
     return fail(CQS_E_UNSUPPORTED, "fp32 path supports D in {32, 64, 96, 128}");
   if (d->qkv_loc == CQS_LOC_DEVICE && d->out_loc != CQS_LOC_DEVICE)
     return fail(CQS_E_UNSUPPORTED, "resident Q/K/V require a device output");
+  if (d->schedule != CQS_SCHED_UNIFORM && d->schedule != CQS_SCHED_HYBRID)
+    return fail(CQS_E_INVALID, "schedule must be CQS_SCHED_UNIFORM or CQS_SCHED_HYBRID");
+  if (d->schedule == CQS_SCHED_HYBRID && d->qkv_loc == CQS_LOC_PINNED_HOST)
+    return fail(CQS_E_UNSUPPORTED, "hybrid schedule: resident plans only (the streamed executor "
+                                   "groups uniform subtrees)");
   return CQS_OK;
 }
 
@@ -325,12 +424,16 @@ cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
   }
   if (chosen < 0)
     return fail(CQS_E_INFEASIBLE, "no divide depth fits budget_bytes under the memory model");
+  if (d.schedule == CQS_SCHED_HYBRID && d.world > 1)
+    if ((st = refine_hybrid(d, I, ls)) != CQS_OK) return st;
 
   auto* p = new cqs_plan_t();
   p->desc = d;
   p->I = I;
   p->desc.offsets = p->I.data();
   p->depth = chosen;
+  p->max_depth = chosen;
+  for (const Task& T : ls.tasks) p->max_depth = std::max(p->max_depth, T.depth);
   p->acc_depth = streamed ? chosen_j : 0;
   p->n_stage_buffers = streamed ? chosen_nbuf : 0;
   p->tasks.swap(ls.tasks);
@@ -341,19 +444,7 @@ cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
   p->max_acc_rows = acc_rows;
   p->total_work = ls.total_work;
 
-  // LPT on exact work (largest first, ties by index) -> least-loaded rank (ties lowest rank).
-  std::vector<int64_t> order;
-  for (int64_t i = 0; i < int64_t(p->tasks.size()); ++i)
-    if (p->tasks[size_t(i)].work > 0) order.push_back(i);
-  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-    return p->tasks[size_t(a)].work > p->tasks[size_t(b)].work;
-  });
-  std::vector<uint64_t> load(size_t(d.world), 0);
-  for (int64_t i : order) {
-    const size_t r = size_t(std::min_element(load.begin(), load.end()) - load.begin());
-    p->tasks[size_t(i)].rank = int32_t(r);
-    load[r] += p->tasks[size_t(i)].work;
-  }
+  lpt_assign(p->tasks, d.world);
   for (int64_t i = 0; i < int64_t(p->tasks.size()); ++i)
     if (p->tasks[size_t(i)].rank == d.rank) {
       p->my_order.push_back(i);
@@ -372,6 +463,7 @@ cqs_status cqs_plan_info(const cqs_plan_t* p, cqs_plan_info_t* info) {
   info->depth = p->depth;
   info->acc_depth = p->acc_depth;
   info->n_stage_buffers = p->n_stage_buffers;
+  info->max_depth = p->max_depth;
   info->n_tasks = int64_t(p->tasks.size());
   info->n_empty = p->n_empty;
   info->max_task_rows = p->max_task_rows;
@@ -392,6 +484,7 @@ cqs_status cqs_plan_task(const cqs_plan_t* p, int64_t idx, cqs_task_t* t) {
   const Task& T = p->tasks[size_t(idx)];
   t->nseg = T.nseg;
   t->rank = T.rank;
+  t->depth = T.depth;
   t->work = T.work;
   std::copy(T.quorum, T.quorum + CQS_MAX_DEPTH, t->quorum);
   for (int a = 0; a < T.nseg; ++a) {
@@ -408,7 +501,8 @@ cqs_status cqs_plan_serialize(const cqs_plan_t* p, void* buf, size_t* len) {
   if (!p || !len) return fail(CQS_E_INVALID, "NULL argument");
   std::string b;
   auto put = [&](const void* x, size_t n) { b.append(static_cast<const char*>(x), n); };
-  const uint32_t ver = 1;
+  const bool mixed = p->max_depth != p->depth;
+  const uint32_t ver = mixed ? 2 : 1;
   b.append("CQSP", 4);
   put(&ver, 4);
   put(&p->desc.N, 8);
@@ -419,13 +513,14 @@ cqs_status cqs_plan_serialize(const cqs_plan_t* p, void* buf, size_t* len) {
   const int64_t nt = int64_t(p->tasks.size());
   put(&nt, 8);
   for (const Task& T : p->tasks) {
+    if (mixed) put(&T.depth, 4);
     put(&T.nseg, 4);
     put(&T.work, 8);
     for (int a = 0; a < T.nseg; ++a) {
       const Seg& s = p->segs[size_t(T.seg_off + a)];
       put(&s.start, 8);
       put(&s.len, 8);
-      put(s.codes, size_t(p->depth));
+      put(s.codes, size_t(T.depth));
     }
     put(T.kept, 4 * size_t(T.nseg));
   }

@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo"):
+def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo", schedule="uniform"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import cqs_synth
@@ -34,7 +34,8 @@ def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo"):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     q, k, v = cqs_synth.torch_qkv(1, H, N, D, 4242, dtype=torch.bfloat16, device="cuda")
-    plan = cqs.cqs_plan(N=N, B=1, H=H, D=D, depth=depth, in_dtype="bf16", world=world, rank=rank)
+    plan = cqs.cqs_plan(N=N, B=1, H=H, D=D, depth=depth, in_dtype="bf16", world=world, rank=rank,
+                        schedule=schedule)
     dev_bytes, _ = cqs.cqs_forward_workspace_size(plan)
     ws = torch.empty(dev_bytes, dtype=torch.uint8, device="cuda")
     out = torch.zeros(1, H, N, D, dtype=torch.bfloat16, device="cuda")
@@ -60,13 +61,15 @@ def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo"):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["gloo", "p2p"])
-@pytest.mark.parametrize("N,depth", [(3000, 2), (2401, 3)])
-def test_two_ranks_one_gpu(N, depth, mode, tmp_path):
+@pytest.mark.parametrize("mode,schedule", [("gloo", "uniform"), ("p2p", "uniform"),
+                                           ("p2p", "hybrid")])
+@pytest.mark.parametrize("N,depth", [(3000, 2), (2401, 3), (5000, 1)])
+def test_two_ranks_one_gpu(N, depth, mode, schedule, tmp_path):
     import cqs_synth
     from oracle import cqs_oracle as O
     world, H, D = 2, 2, 128
-    mp.start_processes(_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path), mode),
+    mp.start_processes(_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path), mode,
+                                      schedule),
                        nprocs=world, start_method="spawn")
     q, k, v = cqs_synth.torch_qkv(1, H, N, D, 4242, dtype=torch.bfloat16)
     Od, ld = O.dense_attention(*(t.double().numpy() for t in (q, k, v)))
@@ -78,7 +81,7 @@ def test_two_ranks_one_gpu(N, depth, mode, tmp_path):
         assert np.abs(l_ - ld[0, :, row0:row0 + rows]).max() <= 1e-3
 
 
-def _bwd_worker(rank, world, port, N, H, D, depth, outdir, mode):
+def _bwd_worker(rank, world, port, N, H, D, depth, outdir, mode, schedule="uniform"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import cqs_synth
@@ -92,7 +95,7 @@ def _bwd_worker(rank, world, port, N, H, D, depth, outdir, mode):
     do = cqs_synth.torch_tensor((1, H, N, D), 4243, "do", torch.bfloat16, "cuda")
     out, lse = cqs.attention(q, k, v, depth=depth)     # O, lse on every rank (as after all-gather)
     plan = cqs.cqs_plan(N=N, B=1, H=H, D=D, depth=depth, in_dtype="bf16", out_dtype="f32",
-                        world=world, rank=rank)
+                        world=world, rank=rank, schedule=schedule)
     bws = torch.empty(cqs.cqs_backward_workspace_size(plan), dtype=torch.uint8, device="cuda")
     cqs.cqs_attention_backward(plan, q, k, v, out, do, lse, None, None, None, 0.0, bws)
     torch.cuda.synchronize()
@@ -115,15 +118,17 @@ def _bwd_worker(rank, world, port, N, H, D, depth, outdir, mode):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["gloo", "p2p"])
+@pytest.mark.parametrize("mode,schedule", [("gloo", "uniform"), ("p2p", "uniform"),
+                                           ("p2p", "hybrid")])
 @pytest.mark.parametrize("N,depth", [(3000, 2), (1030, 1)])
-def test_two_ranks_backward_one_gpu(N, depth, mode, tmp_path):
+def test_two_ranks_backward_one_gpu(N, depth, mode, schedule, tmp_path):
     """Task-sharded backward (each rank its LPT tasks) + one exchange: the owners' row shards of
     dQ/dK/dV match the oracle's dense gradients within R19."""
     import cqs_synth
     from oracle import cqs_oracle as O
     world, H, D = 2, 2, 128
-    mp.start_processes(_bwd_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path), mode),
+    mp.start_processes(_bwd_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path), mode,
+                                          schedule),
                        nprocs=world, start_method="spawn")
     q, k, v = cqs_synth.torch_qkv(1, H, N, D, 4243, dtype=torch.bfloat16)
     do = cqs_synth.torch_tensor((1, H, N, D), 4243, "do", torch.bfloat16)
