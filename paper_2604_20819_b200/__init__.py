@@ -370,3 +370,65 @@ def attention_backward(q, k, v, o, dout, lse, depth=1, scale=0.0, grad_dtype=Non
     dq, dk, dv = (torch.empty((B, H, N, D), dtype=gdt, device=q.device) for _ in range(3))
     st = cqs_attention_backward(p, q, k, v, o, dout, lse, dq, dk, dv, scale, ws, stats=stats)
     return (dq, dk, dv, st) if stats else (dq, dk, dv)
+
+
+def attention_streamed(q, k, v, budget_bytes=0, out_dtype=None, scale=0.0, reserve_bytes=256 << 20,
+                       max_retries=6, offsets=(0, 1, 3), stats=False):
+    """Streamed forward for q, k, v [B,H,N,D] in PINNED HOST memory; O / lse returned in pinned host
+    memory.  OOM guardrail on top of the static plan: the budget defaults to the
+    device's free memory minus `reserve_bytes`, and the planner picks the smallest depth, then
+    fewer staging buffers (the paper's n_cap - 1), that fits.  If allocating the workspace still
+    fails (the budget overstated what the device can give), the budget is re-calibrated from the
+    free memory and the plan is rebuilt at least one level deeper (itr + 1), repeatedly.
+    Returns (out, lse, info[, stats])."""
+    import torch
+    B, H, N, D = q.shape
+    ind = CQS_BF16 if q.dtype == torch.bfloat16 else CQS_F32
+    odt = out_dtype or q.dtype
+
+    def free_budget():
+        return max(int(torch.cuda.mem_get_info()[0]) - int(reserve_bytes), 1)
+
+    budget = int(budget_bytes) if budget_bytes else free_budget()
+    depth = -1
+    for attempt in range(max_retries + 1):
+        try:
+            p = cqs_plan(N=N, B=B, H=H, D=D, depth=depth, budget_bytes=budget, in_dtype=ind,
+                         out_dtype=CQS_BF16 if odt == torch.bfloat16 else CQS_F32,
+                         offsets=offsets, c=len(offsets) * (len(offsets) - 1) + 1,
+                         qkv_loc="host", out_loc="host")
+        except CqsError as e:
+            if e.status == CQS_E_INFEASIBLE and depth >= 0 and attempt < max_retries:
+                depth += 1                        # explicit depth still too big: one more level
+                continue
+            raise
+        info = p.info()
+        dev, host = cqs_forward_workspace_size(p)
+        try:
+            ws = torch.empty(max(dev, 256), dtype=torch.uint8, device="cuda")
+        except torch.cuda.OutOfMemoryError:
+            if attempt == max_retries:
+                raise
+            torch.cuda.empty_cache()
+            budget = min(budget, free_budget())   # calibration from what is really free
+            depth = info.depth + 1                # guardrail: itr + 1 (P:162)
+            continue
+        hws = torch.empty(max(host, 256), dtype=torch.uint8).pin_memory() if host else None
+        out = torch.empty((B, H, N, D), dtype=odt).pin_memory()
+        lse = torch.empty((B, H, N), dtype=torch.float32).pin_memory()
+        try:
+            st = cqs_attention_forward(p, q, k, v, out, lse, scale, 0, ws, hws, stats=stats)
+            torch.cuda.synchronize()
+        except CqsError as e:    # a launch ran out of memory (runtime / module memory)
+            if e.status != CQS_E_CUDA or "out of memory" not in str(e) or attempt == max_retries:
+                raise
+            del ws, hws
+            torch.cuda.empty_cache()
+            budget = min(budget, free_budget())
+            depth = info.depth + 1
+            continue
+        info_d = {"depth": info.depth, "acc_depth": info.acc_depth,
+                  "stage_buffers": info.n_stage_buffers, "attempts": attempt + 1,
+                  "budget_bytes": int(budget), "workspace_bytes": int(dev)}
+        return (out, lse, info_d, st) if stats else (out, lse, info_d)
+    raise CqsError(CQS_E_INFEASIBLE, "guardrail: no plan fits after %d retries" % max_retries)

@@ -98,3 +98,42 @@ def test_streamed_batch2_f32_out():
     out, lse, info, st, peak = run_streamed(q, k, v, budget, depth=2, out_dtype="f32")
     assert info.depth == 2 and peak <= budget + 512
     check(out, lse, q, k, v, 2e-2, 1e-3)
+
+
+def test_guardrail_retries_one_level_deeper():
+    """OOM guardrail: a budget larger than what the device can actually give makes the
+    workspace allocation fail; the call re-plans at itr + 1 and succeeds, matching the oracle."""
+    import numpy as np
+    import torch
+    import cqs_synth
+    import paper_2604_20819_b200 as cqs
+    from oracle import cqs_oracle as O
+    B, H, N, D = 1, 4, 60000, 128
+    q, k, v = (cqs_synth.torch_tensor((B, H, N, D), 61, nm, torch.bfloat16).pin_memory()
+               for nm in ("q", "k", "v"))
+    free = torch.cuda.mem_get_info()[0]
+    # leave ~600 MB free: the depth-0 plan needs ~740 MB of workspace; after calibration (free -
+    # 256 MB reserve) depth 1 with a depth-1 accumulator tier needs ~320 MB
+    blocker = torch.empty(int(free - (600 << 20)), dtype=torch.uint8, device="cuda")
+    try:
+        out, lse, info = cqs.attention_streamed(q, k, v, budget_bytes=1 << 40)
+    finally:
+        del blocker
+        torch.cuda.empty_cache()
+    assert info["attempts"] > 1 and info["depth"] >= 1
+    rows = np.array([0, 4999, 12345, 59999])
+    for h in range(H):
+        Oref, lref = O.dense_attention_rows(q[0, h].double().numpy(), k[0, h].double().numpy(),
+                                            v[0, h].double().numpy(), rows)
+        assert np.abs(out[0, h, rows].double().numpy() - Oref).max() <= 2e-2
+        assert np.abs(lse[0, h, rows].double().numpy() - lref).max() <= 1e-3
+
+
+def test_guardrail_default_budget_from_free_memory():
+    import torch
+    import cqs_synth
+    import paper_2604_20819_b200 as cqs
+    q, k, v = (cqs_synth.torch_tensor((1, 2, 5000, 64), 62, nm, torch.bfloat16).pin_memory()
+               for nm in ("q", "k", "v"))
+    out, lse, info = cqs.attention_streamed(q, k, v)
+    assert info["attempts"] == 1 and info["depth"] == 0 and torch.isfinite(out.float()).all()
