@@ -553,11 +553,22 @@ static cudaError_t launch_bwd_impl(const CUtensorMap* maps, const TaskParams& tp
   return cudaGetLastError();
 }
 
+cudaError_t launch_attn_bwd_fused(const CUtensorMap* maps, const TaskParams& tp, const float* ld,
+                                  int64_t ld_pitch, int64_t N, float* dq, float* dk, float* dv,
+                                  float scale, cudaStream_t st);
+
 // maps: Q, K, V, dO (bf16, 128-row boxes); ld: fp32 [BH][2][pitch] (-lse*log2e, Delta).
+// Default: the dK/dV + dQ kernel pair above.  -DCQS_BWD_FUSED builds route D = 128 through the
+// single fused kernel (attn_bwd_fused_sm100.cu; dQ by fp32 L2 reductions): parity-green but 23%
+// slower on B200 — its red.global traffic (64 KB per 128x128 block) saturates the per-SM L2
+// reduction path (profiles/r01_notes.md).
 cudaError_t launch_attn_bwd_bf16(int D, const CUtensorMap* maps, const TaskParams& tpq,
                                  const TaskParams& tpk, const float* ld, int64_t ld_pitch,
                                  int64_t N, float* dq, float* dk, float* dv, float scale,
                                  cudaStream_t st) {
+#ifdef CQS_BWD_FUSED
+  if (D == 128) return launch_attn_bwd_fused(maps, tpk, ld, ld_pitch, N, dq, dk, dv, scale, st);
+#endif
   if (D == 128) return launch_bwd_impl<128>(maps, tpq, tpk, ld, ld_pitch, N, dq, dk, dv, scale, st);
   if (D == 64) return launch_bwd_impl<64>(maps, tpq, tpk, ld, ld_pitch, N, dq, dk, dv, scale, st);
   return cudaErrorInvalidValue;
