@@ -111,6 +111,8 @@ def test_guardrail_retries_one_level_deeper():
     B, H, N, D = 1, 4, 60000, 128
     q, k, v = (cqs_synth.torch_tensor((B, H, N, D), 61, nm, torch.bfloat16).pin_memory()
                for nm in ("q", "k", "v"))
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()    # cached blocks of earlier tests would otherwise satisfy the alloc
     free = torch.cuda.mem_get_info()[0]
     # leave ~600 MB free: the depth-0 plan needs ~740 MB of workspace; after calibration (free -
     # 256 MB reserve) depth 1 with a depth-1 accumulator tier needs ~320 MB
