@@ -318,10 +318,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #pragma unroll
           for (int u = 0; u < 8; ++u) mx8[u] = s[u];
 #pragma unroll
-          for (int c = 8; c < kBN; c += 16) {
+          for (int c = 8; c + 16 <= kBN; c += 16) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], fmaxf(s[c + u], s[c + 8 + u]));
           }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], s[kBN - 8 + u]);   // last 8 columns
           m = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                     fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
         } else {
@@ -412,13 +414,13 @@ cudaError_t launch_attn_bf16_pair(const CUtensorMap* maps, const TaskParams& tp,
 
 // D = 128 runs on CTA pairs (cta_group::2, 512 query rows per item; K maps with 64-row boxes);
 // D = 64 on single CTAs (256 rows per item).  Callers size work items with attn_rows_per_item
-// and build maps with attn_kv_box_rows.
+// and build the Q / K / V maps with attn_box_rows(D, 0 / 1 / 2).
 #ifndef CQS_ONE_CTA_D128
 int attn_rows_per_item(int D) { return D == 128 ? 512 : 256; }
-int attn_k_box_rows(int D) { return D == 128 ? 64 : 128; }
+int attn_box_rows(int D, int which) { return (D == 128 && which == 1) ? 64 : 128; }
 #else
 int attn_rows_per_item(int) { return 256; }
-int attn_k_box_rows(int) { return 128; }
+int attn_box_rows(int, int) { return 128; }
 #endif
 
 cudaError_t launch_attn_bf16(int D, const CUtensorMap* maps, const TaskParams& tp, float* acc_o,

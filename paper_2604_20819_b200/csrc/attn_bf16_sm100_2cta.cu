@@ -347,10 +347,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
 #pragma unroll
           for (int u = 0; u < 8; ++u) mx8[u] = s[u];
 #pragma unroll
-          for (int c = 8; c < kBN; c += 16) {
+          for (int c = 8; c + 16 <= kBN; c += 16) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], fmaxf(s[c + u], s[c + 8 + u]));
           }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], s[kBN - 8 + u]);   // last 8 columns
           m = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                     fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
         } else {

@@ -28,7 +28,7 @@ cudaError_t launch_attn_f32(int D, const TaskParams& tp, const float* q, const f
                             float scale, cudaStream_t stream);
 cudaError_t launch_fill(float* p, int64_t n, float val, cudaStream_t st);
 int attn_rows_per_item(int D);
-int attn_k_box_rows(int D);
+int attn_box_rows(int D, int which);
 cudaError_t launch_merge(int64_t rows, int B, int H, int D, int n_parts, const float* const* po,
                          const float* const* pl, float* acc_o, float* acc_lse, bool acc_write,
                          void* out, cqs_dtype out_dtype, const int64_t* out_strides,
@@ -181,7 +181,7 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
     for (int i = 0; i < 3; ++i) {
       cqs_status s = make_tmap_bf16(&maps[i], bases[i], d.B, d.H, d.N, d.D, qkv_strides[0],
                                     qkv_strides[1], qkv_strides[2],
-                                    i == 1 ? attn_k_box_rows(d.D) : 128);
+                                    attn_box_rows(d.D, i));
       if (s != CQS_OK) return s;
     }
   }

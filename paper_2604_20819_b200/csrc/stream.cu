@@ -38,7 +38,7 @@ cudaError_t launch_merge(int64_t rows, int B, int H, int D, int n_parts, const f
 cqs_status make_tmap_bf16(CUtensorMap* m, const void* base, int B, int H, int64_t rows, int D,
                           int64_t sB, int64_t sH, int64_t sN, int box_rows);
 int attn_rows_per_item(int D);
-int attn_k_box_rows(int D);
+int attn_box_rows(int D, int which);
 void build_task_params_ext(const cqs_plan_t* p, const Task& T, int rows_per_item,
                            const int64_t* src_rows, const int64_t* dst_rows, TaskParams& tp);
 
@@ -123,7 +123,7 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       for (int t = 0; t < 3; ++t) {
         cqs_status s2 = make_tmap_bf16(&maps[b][t], stage[b][t], d.B, d.H, Lh, d.D,
                                        int64_t(d.H) * Lh * D, Lh * D, D,
-                                       t == 1 ? attn_k_box_rows(d.D) : 128);
+                                       attn_box_rows(d.D, t));
         if (s2 != CQS_OK) return s2;
       }
   const int64_t sstr[4] = {int64_t(d.H) * Lh * D, Lh * D, D, 1};
