@@ -432,3 +432,32 @@ def attention_streamed(q, k, v, budget_bytes=0, out_dtype=None, scale=0.0, reser
                   "budget_bytes": int(budget), "workspace_bytes": int(dev)}
         return (out, lse, info_d, st) if stats else (out, lse, info_d)
     raise CqsError(CQS_E_INFEASIBLE, "guardrail: no plan fits after %d retries" % max_retries)
+
+
+def attention_backward_streamed(q, k, v, o, dout, lse, depth=1, budget_bytes=0, grad_dtype=None,
+                                offsets=(0, 1, 3), max_depth_retries=4, stats=False):
+    """Backward for q, k, v, o, dout ([B,H,N,D] bf16) and lse ([B,H,N] fp32) in PINNED HOST
+    memory; gradients returned in pinned host memory.  If the backward workspace (fp32 gradients
+    of all rows + staging) does not fit `budget_bytes` at `depth`, the next depth is tried.
+    Returns (dq, dk, dv, info[, stats])."""
+    import torch
+    B, H, N, D = q.shape
+    gdt = grad_dtype or q.dtype
+    for attempt in range(max_depth_retries + 1):
+        p = cqs_plan(N=N, B=B, H=H, D=D, depth=depth, budget_bytes=budget_bytes,
+                     in_dtype=CQS_BF16, out_dtype=CQS_BF16 if gdt == torch.bfloat16 else CQS_F32,
+                     offsets=offsets, c=len(offsets) * (len(offsets) - 1) + 1, qkv_loc="host",
+                     out_loc="host")
+        try:
+            need = cqs_backward_workspace_size(p)
+            break
+        except CqsError as e:
+            if e.status != CQS_E_INFEASIBLE or attempt == max_depth_retries:
+                raise
+            depth = p.info().depth + 1
+    ws = torch.empty(max(need, 256), dtype=torch.uint8, device="cuda")
+    dq, dk, dv = (torch.empty((B, H, N, D), dtype=gdt).pin_memory() for _ in range(3))
+    st = cqs_attention_backward(p, q, k, v, o, dout, lse, dq, dk, dv, 0.0, ws, stats=stats)
+    torch.cuda.synchronize()
+    info = {"depth": p.info().depth, "workspace_bytes": int(need)}
+    return (dq, dk, dv, info, st) if stats else (dq, dk, dv, info)

@@ -133,11 +133,12 @@ __global__ void __launch_bounds__(fused::kThreads, 1)
       const int s = i % kStages;
       ptx::mbar_wait(&qd_empty[s], ((i / kStages) & 1) ^ 1);
       const int q_row = cq.row();
+      const int g_row = tp.seg_dst[cq.seg] + cq.kt * 128;            // global row (lse / Delta)
       float* dst = sLD + s * 256 + (lane >> 4) * 128;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int r = (lane & 15) + 16 * u;
-        dst[r] = q_row + r < n_rows ? ld_plane[q_row + r] : 0.f;
+        dst[r] = g_row + r < n_rows ? ld_plane[g_row + r] : 0.f;
       }
       __syncwarp();
       if (lane == 0) {

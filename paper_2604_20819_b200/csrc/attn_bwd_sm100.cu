@@ -194,12 +194,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int s = i % C::kStages;
       ptx::mbar_wait(&qd_empty[s], ((i / C::kStages) & 1) ^ 1);
       uint8_t* st = sStage + s * C::kStageKV;
-      const int q_row = cq.row();
+      const int q_row = cq.row();                                    // TMA (Q / dO) row
+      const int g_row = tp.seg_dst[cq.seg] + cq.kt * 128;            // global row (lse / Delta)
       float* dst = reinterpret_cast<float*>(st + 2 * C::kTile) + (lane >> 4) * 128;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int r = (lane & 15) + 16 * u;
-        dst[r] = q_row + r < n_rows ? ld_plane[q_row + r] : 0.f;
+        dst[r] = g_row + r < n_rows ? ld_plane[g_row + r] : 0.f;
       }
       __syncwarp();
       if (lane == 0) {
@@ -453,7 +454,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t lane_base = uint32_t(sub * 32) << 16;
     const uint32_t tS = tmem + lane_base + C::kColS, tP = tmem + lane_base + C::kColP;
     const uint64_t sc2 = ptx::f2(scale_log2, scale_log2);
-    const int64_t q_row = tp.seg_src[a] + q_off + r;
+    const int64_t q_row = tp.seg_dst[a] + q_off + r;   // global row of the lse / Delta tables
     float nl = 0.f, dl = 0.f;
     if (q_row < n_rows) {
       nl = ld[int64_t(bh) * 2 * ld_pitch + q_row];
@@ -501,8 +502,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 template <int D>
 __global__ void __launch_bounds__(256)
     bwd_prep_kernel(const uint16_t* __restrict__ o, const uint16_t* __restrict__ dO,
-                    int64_t sB, int64_t sH, int64_t sN, const float* __restrict__ lse, int B, int H,
-                    int64_t N, int64_t ld_pitch, float* __restrict__ ld) {
+                    int64_t sB, int64_t sH, int64_t sN, const float* __restrict__ lse,
+                    int64_t lse_pitch, int B, int H, int64_t N, int64_t row0, int64_t ld_pitch,
+                    float* __restrict__ ld) {
   constexpr int kLanes = D / 8;
   const int64_t rows = int64_t(B) * H * N;
   const int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -527,8 +529,8 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int w = kLanes / 2; w > 0; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
   if (row < rows && ch == 0) {
-    ld[bh * 2 * ld_pitch + n] = -lse[row] * 1.4426950408889634f;
-    ld[(bh * 2 + 1) * ld_pitch + n] = acc;
+    ld[bh * 2 * ld_pitch + row0 + n] = -lse[bh * lse_pitch + n] * 1.4426950408889634f;
+    ld[(bh * 2 + 1) * ld_pitch + row0 + n] = acc;
   }
 }
 
@@ -574,9 +576,10 @@ cudaError_t launch_attn_bwd_bf16(int D, const CUtensorMap* maps, const TaskParam
   return cudaErrorInvalidValue;
 }
 
+// rows [row0, row0 + N) of the tables from O / dO rows 0..N of the given views (lse: [B*H][lse_pitch])
 cudaError_t launch_bwd_prep(int D, const void* o, const void* dO, const int64_t* strides,
-                            const float* lse, int B, int H, int64_t N, int64_t ld_pitch, float* ld,
-                            cudaStream_t st) {
+                            const float* lse, int64_t lse_pitch, int B, int H, int64_t N,
+                            int64_t row0, int64_t ld_pitch, float* ld, cudaStream_t st) {
   const int64_t threads = int64_t(B) * H * N * (D / 8);
   const int64_t blocks = (threads + 255) / 256;
   if (blocks <= 0) return cudaSuccess;
@@ -584,10 +587,10 @@ cudaError_t launch_bwd_prep(int D, const void* o, const void* dO, const int64_t*
   auto G = static_cast<const uint16_t*>(dO);
   if (D == 128)
     bwd_prep_kernel<128><<<unsigned(blocks), 256, 0, st>>>(O, G, strides[0], strides[1],
-                                                           strides[2], lse, B, H, N, ld_pitch, ld);
+                                                           strides[2], lse, lse_pitch, B, H, N, row0, ld_pitch, ld);
   else if (D == 64)
     bwd_prep_kernel<64><<<unsigned(blocks), 256, 0, st>>>(O, G, strides[0], strides[1],
-                                                          strides[2], lse, B, H, N, ld_pitch, ld);
+                                                          strides[2], lse, lse_pitch, B, H, N, row0, ld_pitch, ld);
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();

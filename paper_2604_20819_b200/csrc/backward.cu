@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -24,41 +25,87 @@ cudaError_t launch_attn_bwd_bf16(int D, const CUtensorMap* maps, const TaskParam
                                  int64_t N, float* dq, float* dk, float* dv, float scale,
                                  cudaStream_t st);
 cudaError_t launch_bwd_prep(int D, const void* o, const void* dO, const int64_t* strides,
-                            const float* lse, int B, int H, int64_t N, int64_t ld_pitch, float* ld,
-                            cudaStream_t st);
+                            const float* lse, int64_t lse_pitch, int B, int H, int64_t N,
+                            int64_t row0, int64_t ld_pitch, float* ld, cudaStream_t st);
 cudaError_t launch_merge(int64_t rows, int B, int H, int D, int n_parts, const float* const* po,
                          const float* const* pl, float* acc_o, float* acc_lse, bool acc_write,
                          void* out, cqs_dtype out_dtype, const int64_t* out_strides,
                          int64_t out_row0, int64_t n_total, float* lse_out, cudaStream_t st);
 
 struct BwdLayout {
-  int64_t pitch;
-  uint64_t ld, dq, dk, dv, total;
+  int64_t pitch, F = 0;          // lse/Delta row pitch; streamed: rows per chunk buffer
+  int nbuf = 0;                  // streamed: staging buffers
+  uint64_t ld, dq, dk, dv, stage = 0, stage_bytes_per_buf = 0, chunk = 0, chunk_bytes = 0,
+      chunk_lse = 0, total;
 };
 
-static BwdLayout bwd_layout(const cqs_plan_desc& d) {
+// Resident: lse/Delta table [B*H][2][pitch] + three fp32 accumulators [N][B*H][D].
+// Streamed (Q/K/V/O/dO/lse and the gradients in pinned host memory): the same table and
+// accumulators (the whole N stays on the device: accumulator tier j = 0), plus nbuf staging
+// buffers of four tensors [B*H][Lh][D] bf16 (Q, K, V, dO of one task's used segments, Lh = the
+// plan's max_staged_rows) and two chunk buffers of F rows that carry O / dO / lse chunks in (prep
+// pass) and cast gradient chunks out.
+static BwdLayout bwd_layout(const cqs_plan_t* p, int nbuf) {
+  const cqs_plan_desc& d = p->desc;
   BwdLayout L;
-  const int64_t BH = int64_t(d.B) * d.H;
-  L.pitch = (d.N + 3) / 4 * 4;   // 16-byte TMA row pitch
-  const uint64_t acc = align256(uint64_t(d.N) * BH * d.D * 4);
+  const int64_t BH = int64_t(d.B) * d.H, N = d.N, D = d.D;
+  L.pitch = (N + 3) / 4 * 4;   // 16-byte rows
+  const uint64_t acc = align256(uint64_t(N) * BH * D * 4);
   L.ld = 0;
   L.dq = align256(uint64_t(BH) * 2 * L.pitch * 4);
   L.dk = L.dq + acc;
   L.dv = L.dk + acc;
   L.total = L.dv + acc;
+  if (d.qkv_loc == CQS_LOC_PINNED_HOST) {
+    L.nbuf = nbuf;
+    L.stage = L.total;
+    L.stage_bytes_per_buf = 4 * align256(uint64_t(BH) * p->max_staged_rows * D * 2);
+    L.chunk = L.stage + uint64_t(nbuf) * L.stage_bytes_per_buf;
+    int64_t F = (int64_t(64) << 20) / (BH * D * 4);
+    F = std::min<int64_t>(std::max<int64_t>(F, 256), 65536);
+    L.F = std::min<int64_t>(F, N);
+    L.chunk_lse = align256(uint64_t(L.F) * BH * D * 4);
+    L.chunk_bytes = L.chunk_lse + align256(uint64_t(L.F) * BH * 4);
+    L.total = L.chunk + 2 * L.chunk_bytes;
+  }
   return L;
+}
+
+// Streamed plans: two staging buffers if the budget allows, else one, else infeasible.
+static cqs_status bwd_layout_for(const cqs_plan_t* p, BwdLayout* out) {
+  if (p->desc.qkv_loc != CQS_LOC_PINNED_HOST) {
+    *out = bwd_layout(p, 0);
+    return CQS_OK;
+  }
+  const uint64_t budget = p->desc.budget_bytes;
+  for (int nbuf = 2; nbuf >= 1; --nbuf) {
+    BwdLayout L = bwd_layout(p, nbuf);
+    if (budget == 0 || L.total <= budget) {
+      *out = L;
+      return CQS_OK;
+    }
+  }
+  return fail(CQS_E_INFEASIBLE,
+              "streamed backward: fp32 gradients of all N rows + one staging buffer exceed "
+              "budget_bytes at this depth (plan deeper or raise the budget)");
 }
 
 static cqs_status bwd_supported(const cqs_plan_t* p) {
   if (!p) return fail(CQS_E_INVALID, "plan is NULL");
   const cqs_plan_desc& d = p->desc;
-  if (d.qkv_loc != CQS_LOC_DEVICE || d.in_dtype != CQS_BF16)
-    return fail(CQS_E_UNSUPPORTED, "backward runs resident bf16 plans");
+  if (d.in_dtype != CQS_BF16) return fail(CQS_E_UNSUPPORTED, "backward runs bf16 plans");
+  if (d.qkv_loc == CQS_LOC_PINNED_HOST && (d.out_loc != CQS_LOC_PINNED_HOST || d.world != 1))
+    return fail(CQS_E_UNSUPPORTED, "streamed backward: single GPU, gradients in pinned host memory");
   if (d.D != 64 && d.D != 128) return fail(CQS_E_UNSUPPORTED, "backward head dim must be 64 or 128");
   if (int64_t(d.N) * d.B * d.H >= (int64_t(1) << 31))
     return fail(CQS_E_UNSUPPORTED, "backward: N*B*H must stay below 2^31");
   return CQS_OK;
 }
+
+cqs_status backward_streamed(const cqs_plan_t* p, const BwdLayout& L, const void* q, const void* k,
+                             const void* v, const void* o, const void* dout, const float* lse,
+                             void* dq, void* dk, void* dv, float scale, uint8_t* ws,
+                             cudaStream_t st, cqs_stats* stats);
 
 }  // namespace cqs
 
@@ -68,7 +115,9 @@ extern "C" cqs_status cqs_backward_workspace_size(const cqs_plan_t* p, size_t* d
   if (!dev_bytes) return fail(CQS_E_INVALID, "dev_bytes is NULL");
   cqs_status s = bwd_supported(p);
   if (s != CQS_OK) return s;
-  *dev_bytes = size_t(bwd_layout(p->desc).total);
+  BwdLayout L;
+  if ((s = bwd_layout_for(p, &L)) != CQS_OK) return s;
+  *dev_bytes = size_t(L.total);
   return CQS_OK;
 }
 
@@ -77,7 +126,7 @@ extern "C" cqs_status cqs_backward_partial_view(const cqs_plan_t* p, void* dev_w
   if (!dev_ws || !dq || !dk || !dv) return fail(CQS_E_INVALID, "NULL argument");
   cqs_status s = bwd_supported(p);
   if (s != CQS_OK) return s;
-  const BwdLayout L = bwd_layout(p->desc);
+  const BwdLayout L = bwd_layout(p, 0);
   uint8_t* ws = static_cast<uint8_t*>(dev_ws);
   *dq = reinterpret_cast<float*>(ws + L.dq);
   *dk = reinterpret_cast<float*>(ws + L.dk);
@@ -104,8 +153,17 @@ extern "C" cqs_status cqs_attention_backward(const cqs_plan_t* p, const void* q,
     return fail(CQS_E_INVALID, "o/dout must be 16-byte aligned");
   if (scale <= 0.f) scale = 1.f / std::sqrt(float(d.D));
   cudaStream_t st = static_cast<cudaStream_t>(stream_);
+  BwdLayout L;
+  if ((s = bwd_layout_for(p, &L)) != CQS_OK) return s;
+  if (d.qkv_loc == CQS_LOC_PINNED_HOST) {
+    const int64_t c[4] = {int64_t(d.H) * d.N * d.D, int64_t(d.N) * d.D, d.D, 1};
+    for (int i = 0; i < 4; ++i)
+      if (qkv_strides[i] != c[i] || grad_strides[i] != c[i])
+        return fail(CQS_E_INVALID, "streamed backward needs contiguous [B,H,N,D] host tensors");
+    return backward_streamed(p, L, q, k, v, o, dout, lse, dq, dk, dv, scale,
+                             static_cast<uint8_t*>(dev_ws), st, stats);
+  }
   const auto t0 = std::chrono::steady_clock::now();
-  const BwdLayout L = bwd_layout(d);
   uint8_t* ws = static_cast<uint8_t*>(dev_ws);
   float* ld = reinterpret_cast<float*>(ws + L.ld);
   float* acc_dq = reinterpret_cast<float*>(ws + L.dq);
@@ -122,7 +180,8 @@ extern "C" cqs_status cqs_attention_backward(const cqs_plan_t* p, const void* q,
   };
   int64_t launches = 0, run = 0;
   mark();
-  cudaError_t e = launch_bwd_prep(d.D, o, dout, qkv_strides, lse, d.B, d.H, d.N, L.pitch, ld, st);
+  cudaError_t e = launch_bwd_prep(d.D, o, dout, qkv_strides, lse, d.N, d.B, d.H, d.N, 0, L.pitch,
+                                  ld, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(acc_dq, 0, L.total - L.dq, st);
   mark();
   launches += 1;
@@ -186,3 +245,201 @@ extern "C" cqs_status cqs_attention_backward(const cqs_plan_t* p, const void* q,
   }
   return CQS_OK;
 }
+
+// ---------------------------------------------------------------------------------------------
+// Streamed backward (Q, K, V, O, dO, lse and the gradients in pinned host memory).  Same
+// arithmetic as the resident path; the data path follows the streamed forward (stream.cu):
+//   1. prep pass: O / dO / lse rows in chunks of F rows (H2D on a helper stream, double-buffered)
+//      -> Delta and -lse*log2e for every row into the device table (global rows);
+//   2. per task: the used segments of Q, K, V, dO copied into staging buffer (run mod nbuf) on a
+//      copy stream (cudaMemcpy2DAsync, one call per segment per tensor), then the dK/dV and dQ
+//      kernels over TMA maps of that buffer, accumulating into the full-N fp32 gradients;
+//   3. cast pass: fp32 gradient chunks -> out dtype in a chunk buffer -> D2H on a helper stream.
+// ---------------------------------------------------------------------------------------------
+namespace cqs {
+
+#define CKB(x)                                                                       \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) return fail(CQS_E_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+cqs_status backward_streamed(const cqs_plan_t* p, const BwdLayout& L, const void* q, const void* k,
+                             const void* v, const void* o, const void* dout, const float* lse,
+                             void* dq, void* dk, void* dv, float scale, uint8_t* ws,
+                             cudaStream_t st, cqs_stats* stats) {
+  const cqs_plan_desc& d = p->desc;
+  const int64_t N = d.N, D = d.D, BH = int64_t(d.B) * d.H, F = L.F, Lh = p->max_staged_rows;
+  const int64_t e_out = d.out_dtype == CQS_BF16 ? 2 : 4;
+  const int S = L.nbuf;
+  float* ld = reinterpret_cast<float*>(ws + L.ld);
+  float* acc[3] = {reinterpret_cast<float*>(ws + L.dq), reinterpret_cast<float*>(ws + L.dk),
+                   reinterpret_cast<float*>(ws + L.dv)};
+  const uint64_t tens = align256(uint64_t(BH) * Lh * D * 2);
+  uint8_t* stage[2][4];
+  for (int b = 0; b < S; ++b)
+    for (int t = 0; t < 4; ++t) stage[b][t] = ws + L.stage + b * L.stage_bytes_per_buf + t * tens;
+  uint8_t* chunk[2] = {ws + L.chunk, ws + L.chunk + L.chunk_bytes};
+  const uint8_t* hin[4] = {static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k),
+                           static_cast<const uint8_t*>(v), static_cast<const uint8_t*>(dout)};
+  const uint8_t* ho = static_cast<const uint8_t*>(o);
+  uint8_t* hout[3] = {static_cast<uint8_t*>(dq), static_cast<uint8_t*>(dk),
+                      static_cast<uint8_t*>(dv)};
+
+  struct Res {
+    cudaStream_t cs = nullptr, fh = nullptr, fd = nullptr;
+    std::vector<cudaEvent_t> evs;
+    ~Res() {
+      for (auto e : evs) cudaEventDestroy(e);
+      if (cs) cudaStreamDestroy(cs);
+      if (fh) cudaStreamDestroy(fh);
+      if (fd) cudaStreamDestroy(fd);
+    }
+    cudaEvent_t ev() {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      evs.push_back(e);
+      return e;
+    }
+  } R;
+  CKB(cudaStreamCreateWithFlags(&R.cs, cudaStreamNonBlocking));   // staging H2D
+  CKB(cudaStreamCreateWithFlags(&R.fh, cudaStreamNonBlocking));   // chunk H2D
+  CKB(cudaStreamCreateWithFlags(&R.fd, cudaStreamNonBlocking));   // chunk D2H
+  cudaEvent_t c_free[2] = {R.ev(), R.ev()}, c_loaded[2] = {R.ev(), R.ev()},
+              c_done[2] = {R.ev(), R.ev()};
+  cudaEvent_t ev_ready[2] = {R.ev(), R.ev()}, ev_free[2] = {R.ev(), R.ev()};
+  bool buf_used[2] = {false, false};
+  uint64_t h2d = 0, d2h = 0;
+  int64_t launches = 0, run = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  // the helper streams start after everything the caller queued on st
+  {
+    cudaEvent_t start = R.ev();
+    CKB(cudaEventRecord(start, st));
+    CKB(cudaStreamWaitEvent(R.cs, start, 0));
+    CKB(cudaStreamWaitEvent(R.fh, start, 0));
+    CKB(cudaStreamWaitEvent(R.fd, start, 0));
+  }
+
+  // ---- 1. prep: Delta / -lse*log2e for every row ----
+  const int64_t cstr[4] = {int64_t(d.H) * F * D, F * D, D, 1};
+  int cb = 0;
+  for (int64_t r0 = 0; r0 < N; r0 += F, cb ^= 1) {
+    const int64_t n = std::min(F, N - r0);
+    uint8_t* co = chunk[cb];
+    uint8_t* cdo = chunk[cb] + uint64_t(BH) * F * D * 2;
+    float* cl = reinterpret_cast<float*>(chunk[cb] + L.chunk_lse);
+    CKB(cudaStreamWaitEvent(R.fh, c_free[cb], 0));
+    CKB(cudaMemcpy2DAsync(co, size_t(F * D * 2), ho + r0 * D * 2, size_t(N * D * 2),
+                          size_t(n * D * 2), size_t(BH), cudaMemcpyHostToDevice, R.fh));
+    CKB(cudaMemcpy2DAsync(cdo, size_t(F * D * 2), hin[3] + r0 * D * 2, size_t(N * D * 2),
+                          size_t(n * D * 2), size_t(BH), cudaMemcpyHostToDevice, R.fh));
+    CKB(cudaMemcpy2DAsync(cl, size_t(F * 4), lse + r0, size_t(N * 4), size_t(n * 4), size_t(BH),
+                          cudaMemcpyHostToDevice, R.fh));
+    h2d += uint64_t(BH) * n * (2 * D * 2 + 4);
+    CKB(cudaEventRecord(c_loaded[cb], R.fh));
+    CKB(cudaStreamWaitEvent(st, c_loaded[cb], 0));
+    CKB(launch_bwd_prep(int(D), co, cdo, cstr, cl, F, d.B, d.H, n, r0, L.pitch, ld, st));
+    ++launches;
+    CKB(cudaEventRecord(c_free[cb], st));
+  }
+  CKB(cudaMemsetAsync(acc[0], 0, L.stage - L.dq, st));   // the three gradient accumulators
+  // staging rows past a task's last used segment feed masked lanes only; keep them finite
+  CKB(cudaMemsetAsync(ws + L.stage, 0, size_t(S) * L.stage_bytes_per_buf, st));
+  {
+    cudaEvent_t zeroed = R.ev();
+    CKB(cudaEventRecord(zeroed, st));
+    CKB(cudaStreamWaitEvent(R.cs, zeroed, 0));
+  }
+
+  // ---- 2. tasks ----
+  CUtensorMap maps[2][4];
+  for (int b = 0; b < S; ++b)
+    for (int t = 0; t < 4; ++t) {
+      cqs_status s2 = make_tmap_bf16(&maps[b][t], stage[b][t], d.B, d.H, Lh, d.D,
+                                     int64_t(d.H) * Lh * D, Lh * D, D, 128);
+      if (s2 != CQS_OK) return s2;
+    }
+  TaskParams tpq, tpk;
+  for (int64_t ti : p->my_order) {
+    const Task& T = p->tasks[size_t(ti)];
+    const Seg* segs = &p->segs[size_t(T.seg_off)];
+    uint32_t used = 0;
+    for (int a = 0; a < T.nseg; ++a)
+      if (T.kept[a]) used |= (1u << a) | T.kept[a];
+    int64_t src[CQS_MAX_SEGS], dst[CQS_MAX_SEGS], off = 0;
+    for (int a = 0; a < T.nseg; ++a) {
+      src[a] = off;
+      dst[a] = segs[a].start;
+      if (used >> a & 1) off += segs[a].len;
+    }
+    const int b = int(run % S);
+    if (buf_used[b]) CKB(cudaStreamWaitEvent(R.cs, ev_free[b], 0));
+    for (int a = 0; a < T.nseg; ++a) {
+      if (!(used >> a & 1)) continue;
+      for (int t = 0; t < 4; ++t)
+        CKB(cudaMemcpy2DAsync(stage[b][t] + src[a] * D * 2, size_t(Lh * D * 2),
+                              hin[t] + segs[a].start * D * 2, size_t(N * D * 2),
+                              size_t(segs[a].len * D * 2), size_t(BH), cudaMemcpyHostToDevice,
+                              R.cs));
+      h2d += uint64_t(4 * segs[a].len * D * 2 * BH);
+    }
+    CKB(cudaEventRecord(ev_ready[b], R.cs));
+    CKB(cudaStreamWaitEvent(st, ev_ready[b], 0));
+    Task Tt = T;
+    std::memset(Tt.kept, 0, sizeof(Tt.kept));
+    for (int a = 0; a < T.nseg; ++a)
+      for (int c = 0; c < T.nseg; ++c)
+        if (T.kept[a] >> c & 1) Tt.kept[c] |= 1u << a;
+    build_task_params_ext(p, T, 128, src, dst, tpq);
+    build_task_params_ext(p, Tt, 128, src, dst, tpk);
+    CKB(launch_attn_bwd_bf16(int(D), maps[b], tpq, tpk, ld, L.pitch, N, acc[0], acc[1], acc[2],
+                             scale, st));
+    launches += 2;
+    CKB(cudaEventRecord(ev_free[b], st));
+    buf_used[b] = true;
+    ++run;
+  }
+
+  // ---- 3. cast + D2H ----
+  const int64_t ostr[4] = {int64_t(d.H) * F * D, F * D, D, 1};
+  for (int g = 0; g < 3; ++g)
+    for (int64_t r0 = 0; r0 < N; r0 += F, cb ^= 1) {
+      const int64_t n = std::min(F, N - r0);
+      CKB(cudaStreamWaitEvent(st, c_free[cb], 0));
+      CKB(launch_merge(n, d.B, d.H, d.D, 0, nullptr, nullptr, acc[g] + r0 * BH * D, nullptr, false,
+                       chunk[cb], d.out_dtype, ostr, 0, F, nullptr, st));
+      ++launches;
+      CKB(cudaEventRecord(c_done[cb], st));
+      CKB(cudaStreamWaitEvent(R.fd, c_done[cb], 0));
+      CKB(cudaMemcpy2DAsync(hout[g] + r0 * D * e_out, size_t(N * D * e_out), chunk[cb],
+                            size_t(F * D * e_out), size_t(n * D * e_out), size_t(BH),
+                            cudaMemcpyDeviceToHost, R.fd));
+      d2h += uint64_t(BH) * n * D * e_out;
+      CKB(cudaEventRecord(c_free[cb], R.fd));
+    }
+  {   // the caller's stream covers every copy issued on the helper streams
+    cudaEvent_t e1 = R.ev(), e2 = R.ev(), e3 = R.ev();
+    CKB(cudaEventRecord(e1, R.fd));
+    CKB(cudaEventRecord(e2, R.fh));
+    CKB(cudaEventRecord(e3, R.cs));
+    CKB(cudaStreamWaitEvent(st, e1, 0));
+    CKB(cudaStreamWaitEvent(st, e2, 0));
+    CKB(cudaStreamWaitEvent(st, e3, 0));
+  }
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    CKB(cudaStreamSynchronize(st));
+    stats->ms_total =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    stats->bytes_h2d = h2d;
+    stats->bytes_d2h = d2h;
+    stats->tasks_run = run;
+    stats->tasks_skipped = int64_t(p->tasks.size()) - run;
+    stats->kernel_launches = launches;
+    stats->peak_dev_bytes = L.total;
+  }
+  return CQS_OK;
+}
+
+}  // namespace cqs

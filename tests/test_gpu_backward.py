@@ -113,3 +113,44 @@ def test_backward_rejects_unsupported():
     p = cqs.cqs_plan(N=1000, B=1, H=1, D=64, depth=1, in_dtype="f32")
     with pytest.raises(cqs.CqsError):
         cqs.cqs_backward_workspace_size(p)
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("N,depth", [(3000, 1), (2401, 2), (700, 0)])
+def test_streamed_backward_matches_dense_gradients(N, depth, D):
+    """Host-resident Q/K/V/O/dO/lse and gradients: staged per task, same kernels (R19 bar)."""
+    q, k, v, do = inputs(1, 2, N, D, 71 + N + D)
+    out, lse = cqs.attention(q, k, v, depth=depth)
+    hq, hk, hv, ho, hdo = (t.cpu().pin_memory() for t in (q, k, v, out, do))
+    hl = lse.cpu().pin_memory()
+    dq, dk, dv, info = cqs.attention_backward_streamed(hq, hk, hv, ho, hdo, hl, depth=depth,
+                                                       grad_dtype=torch.float32)
+    assert info["depth"] == depth
+    for g, r, nm in zip((dq, dk, dv), ref(q, k, v, do), ("dQ", "dK", "dV")):
+        check_grads(g, r, nm)
+
+
+def test_streamed_backward_budget_one_staging_buffer():
+    """A budget between the one- and two-buffer footprints selects one staging buffer; the
+    measured device peak stays within the budget; results equal the resident backward."""
+    B, H, N, D = 1, 4, 20000, 128
+    q, k, v, do = inputs(B, H, N, D, 5)
+    out, lse = cqs.attention(q, k, v, depth=1)
+    res = cqs.attention_backward(q, k, v, out, do, lse, depth=1, grad_dtype=torch.float32)
+    hq, hk, hv, ho, hdo = (t.cpu().pin_memory() for t in (q, k, v, out, do))
+    hl = lse.cpu().pin_memory()
+    p2 = cqs.cqs_plan(N=N, B=B, H=H, D=D, depth=1, in_dtype="bf16", out_dtype="f32",
+                      qkv_loc="host", out_loc="host")
+    two = cqs.cqs_backward_workspace_size(p2)
+    stage_one = 4 * B * H * cqs.cqs_plan_info(p2).max_staged_rows * D * 2
+    budget = two - stage_one // 2        # fits one staging buffer, not two
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    base = torch.cuda.memory_allocated()
+    dq, dk, dv, info = cqs.attention_backward_streamed(hq, hk, hv, ho, hdo, hl, depth=1,
+                                                       budget_bytes=budget,
+                                                       grad_dtype=torch.float32)
+    peak = torch.cuda.max_memory_allocated() - base
+    assert info["workspace_bytes"] <= budget < two and peak <= budget + 512
+    for a, b in zip((dq, dk, dv), res):
+        assert (a.cuda() - b).abs().max().item() <= 1e-6 * max(1.0, b.abs().max().item())

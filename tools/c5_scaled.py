@@ -94,52 +94,51 @@ def main():
 
 
 def backward(args, q, k, v, out, lse, Np, H, D, N_full, seed):
-    """Table 1's backward half (t7_bwd): Algorithm 2 on the same 7 leaves.  The backward runs
-    resident (Q, K, V, O, dO, lse and the fp32 gradient accumulators in HBM: ~33 GB at N'=14.5M,
-    within one B200's 180 GB; the streamed backward is not built), so its memory is reported, not
-    held to the 16 GiB forward budget."""
+    """Table 1's backward half (t7_bwd): Algorithm 2 on the same 7 leaves, STREAMED like the
+    forward: Q, K, V, O, dO, lse and the gradients in pinned host memory, the fp32 gradient
+    accumulators of all N' rows plus one or two staging buffers on the device, under the same
+    16 GiB budget."""
     import numpy as np
     import torch
     import cqs_synth
     import paper_2604_20819_b200 as cqs
     from oracle import cqs_oracle as O
-    del_list = []
-    qd, kd, vd, od = (t.cuda() for t in (q, k, v, out))
-    ld = lse.cuda()
-    do = cqs_synth.torch_tensor((1, H, Np, D), seed, "do", torch.bfloat16, "cuda")
-    plan = cqs.cqs_plan(N=Np, B=1, H=H, D=D, depth=1, in_dtype="bf16", out_dtype="f32")
+    budget = int(args.budget_gib * (1 << 30))
+    do = cqs_synth.torch_tensor((1, H, Np, D), seed, "do", torch.bfloat16, "cuda").cpu().pin_memory()
+    torch.cuda.empty_cache()
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats()
     base = torch.cuda.memory_allocated()
-    ws = torch.empty(cqs.cqs_backward_workspace_size(plan), dtype=torch.uint8, device="cuda")
-    dq, dk, dv = (torch.empty((1, H, Np, D), dtype=torch.float32, device="cuda") for _ in range(3))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    st = cqs.cqs_attention_backward(plan, qd, kd, vd, od, do, ld, dq, dk, dv, 0.0, ws, stats=True)
+    dq, dk, dv, info, st = cqs.attention_backward_streamed(q, k, v, out, do, lse, depth=1,
+                                                           budget_bytes=budget,
+                                                           grad_dtype=torch.float32, stats=True)
     e1.record()
     torch.cuda.synchronize()
     t7 = e0.elapsed_time(e1) / 1e3
     peak = torch.cuda.max_memory_allocated() - base
     useful = 10.0 * Np * Np * D * H
     rate = useful / t7
-    inputs_bytes = 5 * Np * D * H * 2 + Np * H * 4
     # invariants at any size: sum_j dV_j = sum_i dO_i (rows of P sum to 1); sum_j dK_j = 0
     s_dv, s_do = dv.double().sum(dim=2), do.double().sum(dim=2)
     inv_dv = float((s_dv - s_do).norm() / s_do.norm())
     inv_dk = float(dk.double().sum(dim=2).norm() / dk.double().norm())
     rng = np.random.default_rng(6)
     rows = np.sort(rng.choice(Np, 4, replace=False))
-    f = lambda t: t[0, 0].double().cpu().numpy()
+    f = lambda t: t[0, 0].double().numpy()
     ref = O.dense_dq_rows(f(q), f(k), f(v), f(do), rows, block=1 << 20)
-    got = dq[0, 0, rows].double().cpu().numpy()
+    got = dq[0, 0, rows].double().numpy()
     rel = np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)
-    return {"t7_bwd_s": t7, "useful_tflops_algorithmic": rate / 1e12,
-            "ms_task_kernels": st.ms_attn, "ms_prep_cast": st.ms_merge,
-            "peak_dev_bytes_workspace_and_grads": peak, "input_bytes_resident": inputs_bytes,
+    return {"t7_bwd_s": t7, "useful_tflops_algorithmic": rate / 1e12, "mode": "streamed",
+            "budget_bytes": budget, "workspace_bytes": info["workspace_bytes"],
+            "measured_peak_dev_bytes": peak, "bytes_h2d": st.bytes_h2d, "bytes_d2h": st.bytes_d2h,
             "est_1B_bwd_hours_paper_method": t7 * 7 ** (args.itr - 1) / 3600,
             "est_1B_bwd_hours_by_work": 10.0 * N_full ** 2 * D / rate / 3600,
             "paper_1B_bwd_A100_hours_itr%d" % args.itr: {5: 23411, 6: 30075, 7: 38497, 8: 50556,
                                                           9: 67256}.get(args.itr),
+            "paper_mem_bwd_GiB_itr%d" % args.itr: {5: 41.79, 6: 17.93, 7: 7.68, 8: 3.32,
+                                                    9: 1.43}.get(args.itr),
             "parity_dq_rows": int(len(rows)), "max_dq_row_rel_err": float(rel.max()),
             "invariant_sum_dV_minus_sum_dO_rel": inv_dv, "invariant_sum_dK_rel": inv_dk}
 
