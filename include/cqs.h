@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define CQS_ABI_VERSION 2
+#define CQS_ABI_VERSION 3
 #define CQS_MAX_DEPTH 12   /* N >= 7^depth and N < 2^31 imply depth <= 11 for c = 7           */
 #define CQS_MAX_SEGS 32    /* segments per task; observed <= 8 up to depth 11     */
 
@@ -70,7 +70,13 @@ typedef struct {
                                 tree and split the heaviest leaf into its c children until the LPT
                                 makespan over `world` ranks is within 1% of work/world (or 4096
                                 leaves); a no-op for world = 1.  Leaves then sit at mixed depths. */
-  int32_t reserved;          /* 0 */
+  int32_t n_level_sets;      /* 0: every level uses (c, offsets).  k > 0: divide level t < k uses
+                                interest set t below ("different values of c ... at each
+                                iteration"), deeper levels (c, offsets).  Task count = product of
+                                the levels' c; N must be >= that product (R10).               */
+  const int32_t* level_c;    /* n_level_sets chunk counts, each l(l-1)+1                      */
+  const int32_t* level_offsets; /* concatenated offsets, l_t per level, each a difference set
+                                   with offsets[0] = 0 (host memory, copied by cqs_plan)    */
 } cqs_plan_desc;
 
 #define CQS_SCHED_UNIFORM 0
@@ -124,7 +130,9 @@ cqs_status cqs_plan_task(const cqs_plan_t* plan, int64_t idx, cqs_task_t* task);
  * i32 depth, i64 n_tasks, then per task in lexicographic order: i32 nseg, u64 work,
  * nseg x (i64 start, i64 len, u8 codes[depth]), nseg x u32 kept mask.  A hybrid plan whose
  * leaves differ in depth writes version=2: the same, with i32 leaf depth before each task's nseg
- * and codes[leaf depth] per segment (tasks in DFS order of their quorum paths).
+ * and codes[leaf depth] per segment (tasks in DFS order of their quorum paths).  A plan with
+ * per-level interest sets writes version=3: "CQSP", u32 3, i64 N, i32 depth, i32 L (= deepest
+ * leaf), L x (i32 c_t, i32 l_t, i32 I_t[l_t]), i64 n_tasks, then the version-2 task records.
  * If buf is NULL or *len too small, *len receives the required size and CQS_E_INVALID (buf NULL:
  * CQS_OK) is returned. */
 cqs_status cqs_plan_serialize(const cqs_plan_t* plan, void* buf, size_t* len);

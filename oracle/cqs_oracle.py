@@ -17,6 +17,7 @@ Parts:
   O5  device-memory model (memory_model.py) ....... P:145-162 budget-driven uniform depth (R14)
   O6  backward: dense gradients + literal Alg. 2 .. P:87-128, Appendix D P:429-502 (NEXT-1)
   O7  hybrid scheduling: leaf rule + plan bytes ..... P:154-160 (NEXT-2, reading R20)
+  O8  per-level interest sets (mixed c) ............ P:136 (NEXT-3, reading R21)
 
 Pins (tests/test_oracle_*.py, `-m "not gpu"`): Eq. 1 / Fig. 2 / Fig. 3 facts, brute-force pair
 coverage, closed forms (N=1 -> O=V, Q=K=0 -> mean V), an independent pure-Python loop evaluation,
@@ -130,9 +131,16 @@ class Entry:
 
 def build_subseq_entry(N: int, c: int, I, quorum) -> Entry:
     """Algorithm 3 body for one quorum tuple i = (q_1..q_itr), literally."""
+    return build_subseq_entry_levels(N, [(c, I)] * len(quorum), quorum)
+
+
+def build_subseq_entry_levels(N: int, levels, quorum) -> Entry:
+    """Algorithm 3 body with interest set levels[t] = (c_t, I_t) at iteration t ("different
+    values of c ... can be used at each iteration"; reading R21 — every other step unchanged)."""
     token_ids = np.arange(N, dtype=np.int64)                       # P:276
     label_history, chunks_history = [], []                         # P:277
-    for q_t in quorum:                                             # P:278
+    for t, q_t in enumerate(quorum):
+        c, I = levels[t]
         L = len(token_ids)                                         # P:279
         starts, ends = balanced_chunk_layout(L, c)                 # P:280
         chunks = [(q_t + o) % c for o in I]                        # P:281 (ordered by I, R2)
@@ -263,6 +271,24 @@ def entry_bytes(entry: Entry) -> bytes:
             if kept[a, bb]:
                 m |= 1 << bb
         b += struct.pack("<I", m)
+    return b
+
+
+def quorum_tuples_levels(cs):
+    """All quorum tuples of a tree with c_t children at level t, lexicographic (R3)."""
+    return list(itertools.product(*[range(c) for c in cs]))
+
+
+def plan_bytes_levels(N, levels, itr) -> bytes:
+    """Canonical bytes (version 3, include/cqs.h) of the uniform depth-`itr` tree whose level t
+    uses levels[t] = (c_t, I_t) (R21), from the literal Algorithm 3 of every leaf."""
+    b = PLAN_MAGIC + struct.pack("<I", 3) + struct.pack("<q", N) + struct.pack("<ii", itr, itr)
+    for c, I in levels[:itr]:
+        b += struct.pack("<ii", c, len(I)) + struct.pack("<%di" % len(I), *I)
+    qts = quorum_tuples_levels([c for c, _ in levels[:itr]])
+    b += struct.pack("<q", len(qts))
+    for qt in qts:
+        b += struct.pack("<i", itr) + entry_bytes(build_subseq_entry_levels(N, levels, qt))
     return b
 
 

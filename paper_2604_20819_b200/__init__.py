@@ -49,7 +49,8 @@ class PlanDesc(C.Structure):
                 ("depth", C.c_int32), ("budget_bytes", C.c_uint64), ("in_dtype", C.c_int),
                 ("out_dtype", C.c_int), ("qkv_loc", C.c_int), ("out_loc", C.c_int),
                 ("world", C.c_int32), ("rank", C.c_int32), ("schedule", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("n_level_sets", C.c_int32), ("level_c", C.POINTER(C.c_int32)),
+                ("level_offsets", C.POINTER(C.c_int32))]
 
 
 class PlanInfo(C.Structure):
@@ -150,8 +151,14 @@ def _loc_code(x):
 
 def make_desc(N, B, H, D, depth=1, budget_bytes=0, in_dtype="bf16", out_dtype=None,
               qkv_loc="device", out_loc=None, world=1, rank=0, c=7, offsets=(0, 1, 3),
-              schedule="uniform"):
+              schedule="uniform", levels=None):
+    """levels: optional [(c_t, offsets_t), ...] interest sets for divide levels 0, 1, ...
+    (deeper levels use (c, offsets))."""
     offs = (C.c_int32 * len(offsets))(*offsets)
+    levels = list(levels or [])
+    lc = (C.c_int32 * max(len(levels), 1))(*[int(c_t) for c_t, _ in levels])
+    flat = [int(x) for _, o in levels for x in o]
+    lo = (C.c_int32 * max(len(flat), 1))(*flat)
     d = PlanDesc(N=N, B=B, H=H, D=D, c=c, l=len(offsets), offsets=offs, depth=depth,
                  budget_bytes=int(budget_bytes), in_dtype=_dtype_code(in_dtype),
                  out_dtype=_dtype_code(out_dtype if out_dtype is not None else in_dtype),
@@ -159,8 +166,9 @@ def make_desc(N, B, H, D, depth=1, budget_bytes=0, in_dtype="bf16", out_dtype=No
                  out_loc=_loc_code(out_loc if out_loc is not None else qkv_loc),
                  world=world, rank=rank,
                  schedule={"uniform": CQS_SCHED_UNIFORM, "hybrid": CQS_SCHED_HYBRID}.get(
-                     schedule, schedule))
-    d._offs = offs  # keep alive
+                     schedule, schedule),
+                 n_level_sets=len(levels), level_c=lc, level_offsets=lo)
+    d._offs = (offs, lc, lo)  # keep alive
     return d
 
 

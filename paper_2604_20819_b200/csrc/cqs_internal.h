@@ -27,11 +27,29 @@ struct Task {
   uint32_t kept[CQS_MAX_SEGS] = {};
 };
 
+// Interest sets per divide level ("different values of c ... at each iteration"): level t
+// uses (lc[t], lI[t]) for t < lc.size(), the base (c, I) below that.
+struct Levels {
+  int32_t c = 7;
+  std::vector<int32_t> I;
+  std::vector<int32_t> lc;
+  std::vector<std::vector<int32_t>> lI;
+  int c_at(int t) const { return t < int(lc.size()) ? lc[size_t(t)] : c; }
+  const std::vector<int32_t>& I_at(int t) const { return t < int(lc.size()) ? lI[size_t(t)] : I; }
+  bool mixed() const { return !lc.empty(); }
+  int64_t tasks(int depth) const {   // number of leaves of the uniform depth-`depth` tree
+    int64_t n = 1;
+    for (int t = 0; t < depth; ++t) n *= c_at(t);
+    return n;
+  }
+};
+
 }  // namespace cqs
 
 struct cqs_plan_s {
-  cqs_plan_desc desc;                // offsets pointer re-pointed at I below
-  std::vector<int32_t> I;
+  cqs_plan_desc desc;                // offsets / level pointers re-pointed at lv below
+  cqs::Levels lv;
+  std::vector<int32_t> level_offsets;  // concatenated lv.lI (desc.level_offsets points here)
   int32_t depth = 0;                 // base (uniform) depth; hybrid leaves are at depth >= this
   int32_t max_depth = 0;             // deepest leaf
   int32_t acc_depth = 0;             // streamed mode accumulator tier
@@ -67,6 +85,6 @@ inline int64_t flush_rows(int64_t acc_rows, int64_t BH, int64_t D) {
   return f < acc_rows ? f : acc_rows;
 }
 // Segments of the depth-`depth` subsequence selected by quorum[0..depth) (Alg. 3).
-bool build_segments(int64_t N, int c, const std::vector<int32_t>& I, const int32_t* quorum,
-                    int depth, std::vector<Seg>& out);
+bool build_segments(int64_t N, const Levels& lv, const int32_t* quorum, int depth,
+                    std::vector<Seg>& out);
 }  // namespace cqs

@@ -79,13 +79,15 @@ static inline void chunk_bounds(int64_t L, int c, int u, int64_t* a, int64_t* b)
 
 // Segments of the depth-`depth` subsequence selected by quorum[0..depth).
 // Returns false if more than CQS_MAX_SEGS segments arise.
-bool build_segments(int64_t N, int c, const std::vector<int32_t>& I, const int32_t* quorum,
-                    int depth, std::vector<Seg>& out) {
+bool build_segments(int64_t N, const Levels& lv, const int32_t* quorum, int depth,
+                    std::vector<Seg>& out) {
   std::vector<Seg> cur(1), nxt;
   cur[0].start = 0;
   cur[0].len = N;
   std::memset(cur[0].codes, 0, sizeof(cur[0].codes));
   for (int t = 0; t < depth; ++t) {
+    const int c = lv.c_at(t);
+    const std::vector<int32_t>& I = lv.I_at(t);
     int64_t L = 0;
     for (auto& s : cur) L += s.len;
     nxt.clear();
@@ -150,9 +152,11 @@ static int64_t ipow(int64_t b, int e) {
 }
 
 // Longest depth-j subsequence (rows of one accumulator subtree) — lengths only.
-static int64_t max_node_rows(int64_t N, int c, const std::vector<int32_t>& I, int j) {
+static int64_t max_node_rows(int64_t N, const Levels& lv, int j) {
   std::vector<int64_t> lens{N}, nxt;
   for (int t = 0; t < j; ++t) {
+    const int c = lv.c_at(t);
+    const std::vector<int32_t>& I = lv.I_at(t);
     nxt.clear();
     std::vector<int64_t> uniq(lens);
     std::sort(uniq.begin(), uniq.end());
@@ -181,10 +185,10 @@ struct LeafSet {
 
 // One leaf: segments of the subsequence at path quorum[0..depth), its kept segment-pair blocks,
 // exact work and staged rows (segments touched by a kept block).
-static cqs_status make_leaf(const cqs_plan_desc& d, const std::vector<int32_t>& I,
+static cqs_status make_leaf(const cqs_plan_desc& d, const Levels& lv,
                             const int32_t* quorum, int depth, Task& T, std::vector<Seg>& segs,
                             int64_t* rows_out, int64_t* staged_out) {
-  if (!build_segments(d.N, d.c, I, quorum, depth, segs))
+  if (!build_segments(d.N, lv, quorum, depth, segs))
     return fail(CQS_E_UNSUPPORTED, "task has more than CQS_MAX_SEGS segments");
   T = Task{};
   T.depth = depth;
@@ -220,10 +224,9 @@ static void add_leaf(LeafSet& ls, Task& T, const std::vector<Seg>& segs, int64_t
   ls.tasks.push_back(T);
 }
 
-static cqs_status enumerate_leaves(const cqs_plan_desc& d, const std::vector<int32_t>& I,
-                                   int depth, LeafSet& ls) {
-  const int c = d.c;
-  const int64_t n = ipow(c, depth);
+static cqs_status enumerate_leaves(const cqs_plan_desc& d, const Levels& lv, int depth,
+                                   LeafSet& ls) {
+  const int64_t n = lv.tasks(depth);
   ls = LeafSet{};
   ls.tasks.reserve(size_t(n));
   ls.segs.reserve(size_t(n) * 4);
@@ -232,12 +235,12 @@ static cqs_status enumerate_leaves(const cqs_plan_desc& d, const std::vector<int
   Task T;
   for (int64_t idx = 0; idx < n; ++idx) {
     int64_t r = idx;                                       // lexicographic, q_1 most significant
-    for (int t = depth - 1; t >= 0; --t) {
-      qt[t] = int32_t(r % c);
-      r /= c;
+    for (int t = depth - 1; t >= 0; --t) {                 // (mixed radix for per-level c)
+      qt[t] = int32_t(r % lv.c_at(t));
+      r /= lv.c_at(t);
     }
     int64_t rows, staged;
-    cqs_status st = make_leaf(d, I, qt, depth, T, segs, &rows, &staged);
+    cqs_status st = make_leaf(d, lv, qt, depth, T, segs, &rows, &staged);
     if (st != CQS_OK) return st;
     add_leaf(ls, T, segs, rows, staged);
   }
@@ -270,8 +273,7 @@ static uint64_t lpt_assign(std::vector<Task>& tasks, int world) {
 // decomposition: a node's c children partition its kept pairs (the per-level invariant of CQS
 // Divide), so every ordered pair stays covered exactly once.
 constexpr int64_t kMaxHybridLeaves = 4096;
-static cqs_status refine_hybrid(const cqs_plan_desc& d, const std::vector<int32_t>& I,
-                                LeafSet& ls) {
+static cqs_status refine_hybrid(const cqs_plan_desc& d, const Levels& lv, LeafSet& ls) {
   struct Leaf {
     Task T;
     std::vector<Seg> segs;
@@ -293,20 +295,21 @@ static cqs_status refine_hybrid(const cqs_plan_desc& d, const std::vector<int32_
     for (auto& L : leaves) ts.push_back(L.T);
     const uint64_t span = lpt_assign(ts, d.world);
     if (double(span) <= 1.01 * double(total) / d.world) break;
-    if (int64_t(leaves.size()) + d.c - 1 > kMaxHybridLeaves) break;
     size_t best = 0;
     for (size_t i = 1; i < leaves.size(); ++i)
       if (leaves[i].T.work > leaves[best].T.work) best = i;
     const Task P = leaves[best].T;
+    const int ck = lv.c_at(P.depth);                      // children of a depth-t node: c_t
+    if (int64_t(leaves.size()) + ck - 1 > kMaxHybridLeaves) break;
     if (P.depth + 1 >= CQS_MAX_DEPTH) break;
     // children need at least one token per chunk of the parent's length
-    if (leaves[best].rows < d.c) break;
-    std::vector<Leaf> kids(size_t(d.c));
+    if (leaves[best].rows < ck) break;
+    std::vector<Leaf> kids(static_cast<size_t>(ck));
     int32_t qt[CQS_MAX_DEPTH] = {};
     std::copy(P.quorum, P.quorum + P.depth, qt);
-    for (int q = 0; q < d.c; ++q) {
+    for (int q = 0; q < ck; ++q) {
       qt[P.depth] = q;
-      cqs_status st = make_leaf(d, I, qt, P.depth + 1, kids[size_t(q)].T, kids[size_t(q)].segs,
+      cqs_status st = make_leaf(d, lv, qt, P.depth + 1, kids[size_t(q)].T, kids[size_t(q)].segs,
                                 &kids[size_t(q)].rows, &kids[size_t(q)].staged);
       if (st != CQS_OK) return st;
     }
@@ -328,28 +331,56 @@ extern "C" {
 const char* cqs_last_error(void) { return g_err.c_str(); }
 int32_t cqs_abi_version(void) { return CQS_ABI_VERSION; }
 
-static cqs_status validate_desc(const cqs_plan_desc* d, std::vector<int32_t>& I) {
-  if (!d) return fail(CQS_E_INVALID, "desc is NULL");
-  if (d->N < 1 || d->N > INT32_MAX) return fail(CQS_E_INVALID, "N must be in [1, 2^31)");
-  if (d->B < 1 || d->H < 1 || d->D < 1) return fail(CQS_E_INVALID, "B, H, D must be >= 1");
-  if (d->l < 1 || d->c != d->l * (d->l - 1) + 1)
-    return fail(CQS_E_INVALID, "c must equal l(l-1)+1 (P:30)");
-  if (!d->offsets) return fail(CQS_E_INVALID, "offsets is NULL");
-  I.assign(d->offsets, d->offsets + d->l);
-  for (int i = 0; i < d->l; ++i) {
-    if (I[i] < 0 || I[i] >= d->c) return fail(CQS_E_INVALID, "offset out of [0, c)");
+// One interest set: c = l(l-1)+1, offsets distinct in [0, c), offsets[0] = 0 (R4), and a
+// (c, l, 1) difference set.
+static cqs_status check_set(int c, int l, const int32_t* offs, std::vector<int32_t>& I) {
+  if (l < 1 || c != l * (l - 1) + 1) return fail(CQS_E_INVALID, "c must equal l(l-1)+1 (P:30)");
+  if (!offs) return fail(CQS_E_INVALID, "offsets is NULL");
+  I.assign(offs, offs + l);
+  for (int i = 0; i < l; ++i) {
+    if (I[i] < 0 || I[i] >= c) return fail(CQS_E_INVALID, "offset out of [0, c)");
     for (int j = 0; j < i; ++j)
       if (I[i] == I[j]) return fail(CQS_E_INVALID, "duplicate offset");
   }
   if (I[0] != 0) return fail(CQS_E_INVALID, "offsets[0] must be 0 (owner chunk, R4)");
-  if (!is_difference_set(I, d->c))
+  if (!is_difference_set(I, c))
     return fail(CQS_E_INVALID, "interest set is not a (c,l,1) difference set (P:352)");
+  return CQS_OK;
+}
+
+static int l_of_c(int c) {   // l with l(l-1)+1 = c, or 0
+  for (int l = 1; l * (l - 1) + 1 <= c; ++l)
+    if (l * (l - 1) + 1 == c) return l;
+  return 0;
+}
+
+static cqs_status validate_desc(const cqs_plan_desc* d, Levels& lv) {
+  if (!d) return fail(CQS_E_INVALID, "desc is NULL");
+  if (d->N < 1 || d->N > INT32_MAX) return fail(CQS_E_INVALID, "N must be in [1, 2^31)");
+  if (d->B < 1 || d->H < 1 || d->D < 1) return fail(CQS_E_INVALID, "B, H, D must be >= 1");
+  lv = Levels{};
+  lv.c = d->c;
+  cqs_status st = check_set(d->c, d->l, d->offsets, lv.I);
+  if (st != CQS_OK) return st;
+  if (d->n_level_sets < 0 || d->n_level_sets > CQS_MAX_DEPTH)
+    return fail(CQS_E_INVALID, "n_level_sets out of [0, CQS_MAX_DEPTH]");
+  if (d->n_level_sets > 0 && (!d->level_c || !d->level_offsets))
+    return fail(CQS_E_INVALID, "level_c / level_offsets NULL");
+  for (int t = 0, o = 0; t < d->n_level_sets; ++t) {
+    const int c = d->level_c[t], l = l_of_c(c);
+    if (l == 0) return fail(CQS_E_INVALID, "level c must be l(l-1)+1 (P:30)");
+    std::vector<int32_t> I;
+    if ((st = check_set(c, l, d->level_offsets + o, I)) != CQS_OK) return st;
+    lv.lc.push_back(c);
+    lv.lI.push_back(I);
+    o += l;
+  }
   if (d->world < 1 || d->rank < 0 || d->rank >= d->world)
     return fail(CQS_E_INVALID, "bad world/rank");
   if (d->depth < -1 || d->depth >= CQS_MAX_DEPTH) return fail(CQS_E_INVALID, "bad depth");
-  if (d->depth >= 0 && d->N < ipow(d->c, d->depth))
-    return fail(CQS_E_INVALID, "N < c^depth (R10)");
-  if (d->depth >= 0 && ipow(d->c, d->depth) > kMaxTasks)
+  if (d->depth >= 0 && d->N < lv.tasks(d->depth))
+    return fail(CQS_E_INVALID, "N < c^depth (R10; product of the level c's for mixed trees)");
+  if (d->depth >= 0 && lv.tasks(d->depth) > kMaxTasks)
     return fail(CQS_E_UNSUPPORTED, "more than 7^8 tasks: the plan table would not fit host memory");
   if (d->in_dtype == CQS_BF16 && !(d->D == 64 || d->D == 128))
     return fail(CQS_E_UNSUPPORTED, "bf16 path supports D in {64, 128}");
@@ -367,19 +398,20 @@ static cqs_status validate_desc(const cqs_plan_desc* d, std::vector<int32_t>& I)
 
 cqs_status cqs_memory_model(const cqs_plan_desc* desc, int32_t depth, int32_t acc_depth,
                             int32_t n_stage_buffers, uint64_t* dev_bytes, uint64_t* host_bytes) {
-  std::vector<int32_t> I;
-  cqs_status st = validate_desc(desc, I);
+  Levels lv;
+  cqs_status st = validate_desc(desc, lv);
   if (st != CQS_OK) return st;
-  if (depth < 0 || acc_depth < 0 || acc_depth > depth || desc->N < ipow(desc->c, depth))
+  if (depth < 0 || depth >= CQS_MAX_DEPTH || acc_depth < 0 || acc_depth > depth ||
+      desc->N < lv.tasks(depth))
     return fail(CQS_E_INVALID, "bad depth / acc_depth");
   LeafSet ls;
   int64_t staged = desc->N;
   if (desc->qkv_loc == CQS_LOC_PINNED_HOST) {
-    if ((st = enumerate_leaves(*desc, I, depth, ls)) != CQS_OK) return st;
+    if ((st = enumerate_leaves(*desc, lv, depth, ls)) != CQS_OK) return st;
     staged = ls.max_staged;
   }
   const int64_t acc_rows =
-      desc->qkv_loc == CQS_LOC_PINNED_HOST ? max_node_rows(desc->N, desc->c, I, acc_depth) : desc->N;
+      desc->qkv_loc == CQS_LOC_PINNED_HOST ? max_node_rows(desc->N, lv, acc_depth) : desc->N;
   MemModel m = memory_model(*desc, staged, acc_rows, n_stage_buffers);
   if (dev_bytes) *dev_bytes = m.caller_dev + m.dev_ws;
   if (host_bytes) *host_bytes = m.host_ws;
@@ -389,16 +421,16 @@ cqs_status cqs_memory_model(const cqs_plan_desc* desc, int32_t depth, int32_t ac
 cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
   if (!out) return fail(CQS_E_INVALID, "out is NULL");
   *out = nullptr;
-  std::vector<int32_t> I;
-  cqs_status st = validate_desc(desc, I);
+  Levels lv;
+  cqs_status st = validate_desc(desc, lv);
   if (st != CQS_OK) return st;
   const cqs_plan_desc& d = *desc;
   const bool streamed = d.qkv_loc == CQS_LOC_PINNED_HOST;
   const uint64_t budget = d.budget_bytes;
 
   int max_depth = 0;
-  while (max_depth + 1 < CQS_MAX_DEPTH && ipow(d.c, max_depth + 1) <= d.N &&
-         ipow(d.c, max_depth + 1) <= kMaxTasks)
+  while (max_depth + 1 < CQS_MAX_DEPTH && lv.tasks(max_depth + 1) <= d.N &&
+         lv.tasks(max_depth + 1) <= kMaxTasks)
     ++max_depth;
   const int k_lo = d.depth >= 0 ? d.depth : 0, k_hi = d.depth >= 0 ? d.depth : max_depth;
 
@@ -407,7 +439,7 @@ cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
   int64_t acc_rows = d.N;
   MemModel mm{};
   for (int k = k_lo; k <= k_hi && chosen < 0; ++k) {
-    if ((st = enumerate_leaves(d, I, k, ls)) != CQS_OK) return st;
+    if ((st = enumerate_leaves(d, lv, k, ls)) != CQS_OK) return st;
     if (!streamed) {
       mm = memory_model(d, 0, d.N, 0);
       if (budget == 0 || mm.caller_dev + mm.dev_ws <= budget) chosen = k;
@@ -415,7 +447,7 @@ cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
     }
     for (int nbuf = 2; nbuf >= 1 && chosen < 0; --nbuf)
       for (int j = 0; j <= k && chosen < 0; ++j) {
-        const int64_t rows = max_node_rows(d.N, d.c, I, j);
+        const int64_t rows = max_node_rows(d.N, lv, j);
         MemModel m = memory_model(d, ls.max_staged, rows, nbuf);
         if (budget == 0 || m.caller_dev + m.dev_ws <= budget) {
           chosen = k, chosen_j = j, chosen_nbuf = nbuf, acc_rows = rows, mm = m;
@@ -425,12 +457,16 @@ cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
   if (chosen < 0)
     return fail(CQS_E_INFEASIBLE, "no divide depth fits budget_bytes under the memory model");
   if (d.schedule == CQS_SCHED_HYBRID && d.world > 1)
-    if ((st = refine_hybrid(d, I, ls)) != CQS_OK) return st;
+    if ((st = refine_hybrid(d, lv, ls)) != CQS_OK) return st;
 
   auto* p = new cqs_plan_t();
   p->desc = d;
-  p->I = I;
-  p->desc.offsets = p->I.data();
+  p->lv = lv;
+  p->desc.offsets = p->lv.I.data();
+  // the plan owns its level tables (the caller's arrays may go away)
+  for (auto& I : p->lv.lI) p->level_offsets.insert(p->level_offsets.end(), I.begin(), I.end());
+  p->desc.level_c = p->lv.lc.empty() ? nullptr : p->lv.lc.data();
+  p->desc.level_offsets = p->level_offsets.empty() ? nullptr : p->level_offsets.data();
   p->depth = chosen;
   p->max_depth = chosen;
   for (const Task& T : ls.tasks) p->max_depth = std::max(p->max_depth, T.depth);
@@ -501,19 +537,33 @@ cqs_status cqs_plan_serialize(const cqs_plan_t* p, void* buf, size_t* len) {
   if (!p || !len) return fail(CQS_E_INVALID, "NULL argument");
   std::string b;
   auto put = [&](const void* x, size_t n) { b.append(static_cast<const char*>(x), n); };
-  const bool mixed = p->max_depth != p->depth;
-  const uint32_t ver = mixed ? 2 : 1;
+  // v1: uniform tree; v2: hybrid (leaves of mixed depth); v3: per-level interest sets
+  const bool mixed_depth = p->max_depth != p->depth, levels = p->lv.mixed();
+  const uint32_t ver = levels ? 3 : (mixed_depth ? 2 : 1);
+  const bool per_task_depth = ver >= 2;
   b.append("CQSP", 4);
   put(&ver, 4);
   put(&p->desc.N, 8);
-  put(&p->desc.c, 4);
-  put(&p->desc.l, 4);
-  put(p->I.data(), 4 * p->I.size());
-  put(&p->depth, 4);
+  if (ver == 3) {
+    put(&p->depth, 4);
+    const int32_t nl = p->max_depth;          // the level table covers every leaf's levels
+    put(&nl, 4);
+    for (int t = 0; t < nl; ++t) {
+      const int32_t c = p->lv.c_at(t), l = int32_t(p->lv.I_at(t).size());
+      put(&c, 4);
+      put(&l, 4);
+      put(p->lv.I_at(t).data(), 4 * size_t(l));
+    }
+  } else {
+    put(&p->desc.c, 4);
+    put(&p->desc.l, 4);
+    put(p->lv.I.data(), 4 * p->lv.I.size());
+    put(&p->depth, 4);
+  }
   const int64_t nt = int64_t(p->tasks.size());
   put(&nt, 8);
   for (const Task& T : p->tasks) {
-    if (mixed) put(&T.depth, 4);
+    if (per_task_depth) put(&T.depth, 4);
     put(&T.nseg, 4);
     put(&T.work, 8);
     for (int a = 0; a < T.nseg; ++a) {

@@ -192,7 +192,7 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
     while (ge < nmy &&
            std::equal(T0.quorum, T0.quorum + j, p->tasks[size_t(p->my_order[size_t(ge)])].quorum))
       ++ge;
-    build_segments(N, d.c, p->I, T0.quorum, j, node);
+    build_segments(N, p->lv, T0.quorum, j, node);
     std::vector<int64_t> node_off(node.size());
     int64_t node_rows = 0;
     for (size_t i = 0; i < node.size(); ++i) node_off[i] = node_rows, node_rows += node[i].len;

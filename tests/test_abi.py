@@ -18,11 +18,11 @@ def test_header_symbols_exported():
     L = ctypes.CDLL(cqs.LIB_PATH)
     for name in declared:
         assert hasattr(L, name), name
-    assert cqs.lib().cqs_abi_version() == 2
+    assert cqs.lib().cqs_abi_version() == 3
 
 
 def test_struct_sizes_match_c_layout():
-    assert ctypes.sizeof(cqs.PlanDesc) == 88
+    assert ctypes.sizeof(cqs.PlanDesc) == 104
     assert ctypes.sizeof(cqs.PlanInfo) == 96
 
 

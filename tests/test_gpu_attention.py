@@ -195,3 +195,18 @@ def test_bf16_other_interest_sets(c, I, N, depth):
     out, lse = cqs.attention(q, k, v, depth=depth, offsets=I)
     torch.cuda.synchronize()
     check_bf16(out, lse, *ref_dense(q, k, v))
+
+
+@pytest.mark.parametrize("levels,N,depth", [([(7, (0, 1, 3)), (13, (0, 1, 3, 9))], 3000, 2),
+                                            ([(13, (0, 1, 3, 9)), (7, (0, 1, 5))], 2500, 2)])
+def test_bf16_mixed_level_interest_sets(levels, N, depth):
+    """NEXT-3: a different c per divide level through the same kernels."""
+    q, k, v = gen(1, 2, N, 128, 500 + N, bf16=True)
+    p = cqs.cqs_plan(N=N, B=1, H=2, D=128, depth=depth, in_dtype="bf16", levels=levels)
+    dev, _ = cqs.cqs_forward_workspace_size(p)
+    ws = torch.empty(dev, dtype=torch.uint8, device=DEV)
+    out = torch.empty_like(q)
+    lse = torch.empty((1, 2, N), dtype=torch.float32, device=DEV)
+    cqs.cqs_attention_forward(p, q, k, v, out, lse, 0.0, 0, ws, None)
+    torch.cuda.synchronize()
+    check_bf16(out, lse, *ref_dense(q, k, v))

@@ -139,3 +139,28 @@ def test_guardrail_default_budget_from_free_memory():
                for nm in ("q", "k", "v"))
     out, lse, info = cqs.attention_streamed(q, k, v)
     assert info["attempts"] == 1 and info["depth"] == 0 and torch.isfinite(out.float()).all()
+
+
+def test_streamed_mixed_level_interest_sets():
+    """Per-level interest sets in the streamed executor (staging + accumulator tier)."""
+    import numpy as np
+    import torch
+    import cqs_synth
+    import paper_2604_20819_b200 as cqs
+    from oracle import cqs_oracle as O
+    B, H, N, D = 1, 2, 3000, 128
+    q, k, v = (cqs_synth.torch_tensor((B, H, N, D), 64, nm, torch.bfloat16).pin_memory()
+               for nm in ("q", "k", "v"))
+    levels = [(13, (0, 1, 3, 9)), (7, (0, 1, 3))]
+    p = cqs.cqs_plan(N=N, B=B, H=H, D=D, depth=2, in_dtype="bf16", qkv_loc="host",
+                     out_loc="host", levels=levels)
+    dev, host = cqs.cqs_forward_workspace_size(p)
+    ws = torch.empty(max(dev, 256), dtype=torch.uint8, device="cuda")
+    hws = torch.empty(max(host, 256), dtype=torch.uint8).pin_memory() if host else None
+    out = torch.empty((B, H, N, D), dtype=torch.bfloat16).pin_memory()
+    lse = torch.empty((B, H, N), dtype=torch.float32).pin_memory()
+    cqs.cqs_attention_forward(p, q, k, v, out, lse, 0.0, 0, ws, hws)
+    torch.cuda.synchronize()
+    Od, ld = O.dense_attention(*(t.double().numpy() for t in (q, k, v)))
+    assert np.abs(out.double().numpy() - Od).max() <= 2e-2
+    assert np.abs(lse.double().numpy() - ld).max() <= 1e-3
