@@ -362,7 +362,24 @@ def main():
         f1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = f0.elapsed_time(f1) / n_e2e
-        e2e = {"value": flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+        # host link reference (SURVEY §8d "Streaming: host link"): pinned 1 GiB, best of 3
+        link = {}
+        hb = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
+        db = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+        for name, fn in (("h2d_gbs", lambda: db.copy_(hb, non_blocking=True)),
+                         ("d2h_gbs", lambda: hb.copy_(db, non_blocking=True))):
+            best = 1e9
+            for _ in range(3):
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record()
+                fn()
+                a1.record()
+                torch.cuda.synchronize()
+                best = min(best, a0.elapsed_time(a1))
+            link[name] = (1 << 30) / (best * 1e-3) / 1e9
+        del hb, db
+        e2e = {"value": flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "host_link": link,
+               "h2d_achieved_gbs": h2d / (e2e_ms * 1e-3) / 1e9,
                "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "path": "cqs_attention_forward with Q/K/V/O/lse in pinned host memory (streamed)",
                "acc_depth": ps.info().acc_depth, "stage_buffers": ps.info().n_stage_buffers}
