@@ -30,6 +30,15 @@
 namespace cqs {
 
 constexpr int kAttnThreads = 384;
+
+#ifdef CQS_DBG_TIMING   // timing experiment only (tools/timing_probe.py --d64)
+__device__ unsigned long long g_cqs_dbg1[16];
+#define DBG1_T0(v) const long long v = clock64()
+#define DBG1_ADD(i, x) atomicAdd(&g_cqs_dbg1[i], (unsigned long long)(x))
+#else
+#define DBG1_T0(v)
+#define DBG1_ADD(i, x) ((void)0)
+#endif
 constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
 // column pairs (i mod 8) whose exp2 runs on the FMA pipe instead of MUFU
 // (measured on B200, C2 shape, fused exp loop: MUFU-only is fastest at both head dims — D=64:
@@ -40,6 +49,16 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
 template <int D> constexpr uint32_t kPolyMask = CQS_DBG_POLY_MASK;
 #else
 template <int D> constexpr uint32_t kPolyMask = 0x0;
+#endif
+
+// Warpgroup ping-pong of the two tiles' softmax phases (named barriers 1 / 2).  Off: measured
+// slower at both head dims (D = 64: 651 vs 735 TFLOP/s; cycle counters in profiles/r01_notes.md).
+#ifdef CQS_DBG_PINGPONG
+template <int D>
+constexpr bool kPingPong = true;
+#else
+template <int D>
+constexpr bool kPingPong = false;
 #endif
 
 template <int D>
@@ -185,6 +204,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                             (acc || ks > 0));
         ptx::mma_commit_elect(&o_bar[t]);
       };
+      DBG1_T0(tm0);
+      long long mma_pwait = 0, mma_kvwait = 0;
+      (void)mma_pwait;
+      (void)mma_kvwait;
       int it = 0;
       ptx::mbar_wait(q_full, 0);
       const int sK0 = it % C::kStages;
@@ -205,15 +228,25 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           ++it;
         }
         const int sV = it % C::kStages;
+        DBG1_T0(tk0);
 #ifdef CQS_DBG_NO_TMA_REFILL
         if (it < C::kStages)
 #endif
         ptx::mbar_wait(&kv_full[sV], (it / C::kStages) & 1);
+        DBG1_T0(tk1);
+#ifdef CQS_DBG_TIMING
+        mma_kvwait += tk1 - tk0;
+#endif
         ++it;
         ptx::tc_fence_after();
         for (int t = 0; t < (two ? 2 : 1); ++t) {
 #ifndef CQS_DBG_NO_PWAIT
+          DBG1_T0(tw0);
           ptx::mbar_wait(&p_full[t], j & 1);
+          DBG1_T0(tw1);
+#ifdef CQS_DBG_TIMING
+          mma_pwait += tw1 - tw0;
+#endif
 #endif
           ptx::tc_fence_after();
           issue_PV(t, sV, j > 0);
@@ -222,6 +255,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         ptx::mma_commit_elect(&kv_empty[sV]);
         if (sKn >= 0) ptx::mma_commit_elect(&kv_empty[sKn]);
       }
+      DBG1_T0(tm1);
+      if (lane == 0) DBG1_ADD(5, tm1 - tm0), DBG1_ADD(6, n_kv), DBG1_ADD(4, mma_pwait),
+                     DBG1_ADD(3, mma_kvwait);
       // drain: q_full's second phase completes when every MMA of this CTA has retired
       ptx::mma_commit_elect(q_full);
       ptx::mbar_wait(q_full, 1);
@@ -243,11 +279,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       for (int j = 0; j < n_kv; ++j) {
         const int valid = cur.valid();
         cur.next();
+        DBG1_T0(ts0);
         ptx::mbar_wait(&s_full[t], j & 1);
         ptx::tc_fence_after();
+        DBG1_T0(ts1);
 #ifdef CQS_DBG_NO_PWAIT   // timing experiment only: softmax warps do nothing
         break;
 #endif
+        if (kPingPong<D> && two && !(t == 0 && j == 0)) ptx::named_bar_sync(1 + t, 256);
 #ifdef CQS_DBG_SKIP_SOFTMAX   // timing experiment only: tensor/TMA pipeline without softmax work
         if (j == 0) m = 0.f, l = 1.f;
         ptx::tc_fence_before();
@@ -360,6 +399,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+        if (kPingPong<D> && two && !(t == 1 && j == n_kv - 1)) ptx::named_bar_arrive(2 - t, 256);
+#ifdef CQS_DBG_TIMING
+        DBG1_T0(ts2);
+        if (lane == 0) DBG1_ADD(0, ts1 - ts0), DBG1_ADD(1, ts2 - ts1), DBG1_ADD(2, 1);
+#endif
       }
       // ---- epilogue: O_i = O / l, lse_i = ln(sum exp) -> merge into the accumulator ----
       ptx::mbar_wait(&o_bar[t], (n_kv - 1) & 1);
@@ -435,3 +479,13 @@ cudaError_t launch_attn_bf16(int D, const CUtensorMap* maps, const TaskParams& t
 }
 
 }  // namespace cqs
+
+#ifdef CQS_DBG_TIMING
+extern "C" int cqs_dbg1_read(unsigned long long* out, int n) {
+  return int(cudaMemcpyFromSymbol(out, cqs::g_cqs_dbg1, sizeof(unsigned long long) * (n < 16 ? n : 16)));
+}
+extern "C" int cqs_dbg1_reset() {
+  unsigned long long z[16] = {};
+  return int(cudaMemcpyToSymbol(cqs::g_cqs_dbg1, z, sizeof(z)));
+}
+#endif
