@@ -95,7 +95,10 @@ def ncu_traffic(kernel_prefix):
     summary (profiles/), or None."""
     import glob
     best = None
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_summary.json"))):
+    # the "_final_" capture (the kernel as committed) wins over earlier captures of the same kernel
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_summary.json")),
+                   key=lambda f: ("_final_" in os.path.basename(f), f))
+    for f in files:
         try:
             for d in json.load(open(f)):
                 if d["kernel"].startswith(kernel_prefix) or kernel_prefix in d["kernel"]:
