@@ -92,3 +92,20 @@ def choose(N, B, H, D, e_in, e_out, streamed, out_host, budget, c=7, I=(0, 1, 3)
                 if budget == 0 or b <= budget:
                     return k, j, nbuf, b
     return None
+
+
+# ---- backward (Algorithm 2, NEXT-1) device workspace: this build's accounting (DESIGN.md
+#      "Backward kernels"); the paper only reports Mem_bwd ~ 2 x Mem_fwd ----
+
+def backward_workspace_bytes(N, BH, D, streamed=False, staged_rows=0, nbuf=0):
+    """lse/Delta table [BH][2][ceil4(N)] fp32 + three fp32 gradient accumulators [N][BH][D];
+    streamed adds nbuf staging buffers of four bf16 tensors [BH][staged_rows][D] and two chunk
+    buffers of F rows (F = clamp(64 MiB / (BH D 4), 256, 65536), at most N) holding F x BH x D
+    fp32 + F x BH fp32 each."""
+    pitch = (N + 3) // 4 * 4
+    b = _a256(BH * 2 * pitch * 4) + 3 * _a256(N * BH * D * 4)
+    if streamed:
+        b += nbuf * 4 * _a256(BH * staged_rows * D * 2)
+        F = min(max((64 << 20) // (BH * D * 4), 256), 65536, N)
+        b += 2 * (_a256(F * BH * D * 4) + _a256(F * BH * 4))
+    return b

@@ -70,3 +70,22 @@ def test_resident_c2_bytes():
     info = cqs.cqs_plan(_desc(131072, 1, 32, 128, False, 0, depth=1)).info()
     assert info.predicted_peak_bytes == M.device_bytes(131072, 1, 32, 128, 2, 2, False, False, 0,
                                                        131072, 0)
+
+
+@pytest.mark.parametrize("N,B,H,D", [(131072, 1, 32, 128), (1030, 2, 3, 64), (14458261, 1, 1, 64)])
+def test_backward_workspace_matches_c_abi(N, B, H, D):
+    """cqs_backward_workspace_size (resident) equals the oracle's byte model; and the streamed
+    figure equals it with the plan's staged rows and the staging-buffer count the budget allows."""
+    import paper_2604_20819_b200 as cqs
+    from oracle import memory_model as M
+    p = cqs.cqs_plan(N=N, B=B, H=H, D=D, depth=1, in_dtype="bf16")
+    assert cqs.cqs_backward_workspace_size(p) == M.backward_workspace_bytes(N, B * H, D)
+    ps = cqs.cqs_plan(N=N, B=B, H=H, D=D, depth=1, in_dtype="bf16", qkv_loc="host",
+                      out_loc="host")
+    Lh = ps.info().max_staged_rows
+    two = M.backward_workspace_bytes(N, B * H, D, True, Lh, 2)
+    assert cqs.cqs_backward_workspace_size(ps) == two
+    one = M.backward_workspace_bytes(N, B * H, D, True, Lh, 1)
+    assert one < two
+    if N == 14458261:   # the C5 scaled backward under 16 GiB takes one staging buffer (14.43 GB)
+        assert one <= 16 << 30 < two
