@@ -69,6 +69,15 @@ struct AttnCfg {
   static constexpr int kStages = D == 128 ? 4 : 8;
   static constexpr int kSmemBytes = 2 * kQBytes + kStages * kKVBytes + 1024 + 512;
   static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
+  // D = 64: Q lives in TMEM (A operand of S = Q K^T from TMEM, kind::f16 packed like P), so the
+  // S MMA reads only K from shared memory (an SS MMA at M = N = 128 needs the full 128 B/clk of
+  // SMEM bandwidth, leaving none for the TMA fills).  D = 128 has no free TMEM columns for it.
+#ifdef CQS_DBG_Q_SMEM
+  static constexpr bool kQInTmem = false;
+#else
+  static constexpr bool kQInTmem = D == 64;
+#endif
+  static constexpr uint32_t kColQ0 = 256 + 2 * D, kColQ1 = 256 + 2 * D + D / 2;
 };
 
 template <int D>
@@ -91,7 +100,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t* s_full = kv_empty + C::kStages;   // 2
   uint64_t* p_full = s_full + 2;              // 2
   uint64_t* o_bar = p_full + 2;               // 2
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + 2);
+  uint64_t* q_tm = o_bar + 2;                 // 1: Q copied into TMEM (kQInTmem)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_tm + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -111,6 +121,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   const uint32_t kmask = tp.kept[a];
   int n_kv = 0;
   for (uint32_t m = kmask; m; m &= m - 1) n_kv += (tp.seg_len[__ffs(m) - 1] + kBN - 1) / kBN;
+  const int kv0 = kv_start(item, n_kv);
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(q_full, 1);
@@ -123,6 +134,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       ptx::mbar_init(&p_full[t], 4);
       ptx::mbar_init(&o_bar[t], 1);
     }
+    ptx::mbar_init(q_tm, two ? 8 : 4);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
@@ -163,8 +175,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         ++it;
       };
       KvCursor ck, cv;
-      ck.init(&tp, kmask);
-      cv.init(&tp, kmask);
+      ck.init(&tp, kmask, kv0);
+      cv.init(&tp, kmask, kv0);
       load(&tmK, ck.row());
       ck.next();
       for (int j = 0; j < n_kv; ++j) {
@@ -191,7 +203,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off = ((ks >> 2) * (kBM * 128) + (ks & 3) * 32) >> 4;
-          ptx::mma_ss_elect(d, qa + off, kb + off, idesc_qk, ks > 0);
+          if constexpr (C::kQInTmem)
+            ptx::mma_ts_elect(d, tmem + (t ? C::kColQ1 : C::kColQ0) + ks * 8, kb + off, idesc_qk,
+                              ks > 0);
+          else
+            ptx::mma_ss_elect(d, qa + off, kb + off, idesc_qk, ks > 0);
         }
         ptx::mma_commit_elect(&s_full[t]);
       };
@@ -209,7 +225,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       (void)mma_pwait;
       (void)mma_kvwait;
       int it = 0;
-      ptx::mbar_wait(q_full, 0);
+      ptx::mbar_wait(C::kQInTmem ? q_tm : q_full, 0);
       const int sK0 = it % C::kStages;
       ptx::mbar_wait(&kv_full[sK0], (it / C::kStages) & 1);
       ++it;
@@ -274,8 +290,25 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t tS = tmem + lane_base + (t ? C::kColS1 : C::kColS0);
       const uint32_t tO = tmem + lane_base + (t ? C::kColO1 : C::kColO0);
       float m = -INFINITY, l = 0.f;
+      if constexpr (C::kQInTmem) {
+        // this thread's Q row (SW128 TMA box: 16-byte chunk c of row r sits at chunk c ^ (r & 7))
+        // -> 32 packed bf16 pairs -> TMEM columns kColQ_t (same packing as P)
+        ptx::mbar_wait(q_full, 0);
+        const uint8_t* qrow = sQ + t * C::kQBytes + r * 128;
+        uint32_t qv[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 u = *reinterpret_cast<const uint4*>(qrow + ((c ^ (r & 7)) << 4));
+          qv[4 * c + 0] = u.x, qv[4 * c + 1] = u.y, qv[4 * c + 2] = u.z, qv[4 * c + 3] = u.w;
+        }
+        ptx::tmem_st32(tmem + lane_base + (t ? C::kColQ1 : C::kColQ0), qv);
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(q_tm);
+      }
       KvCursor cur;
-      cur.init(&tp, kmask);
+      cur.init(&tp, kmask, kv0);
       for (int j = 0; j < n_kv; ++j) {
         const int valid = cur.valid();
         cur.next();
@@ -455,17 +488,34 @@ static cudaError_t launch_bf16_impl(const CUtensorMap* maps, const TaskParams& t
 
 cudaError_t launch_attn_bf16_pair(const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
                                   float* acc_lse, float scale, cudaStream_t stream);
+cudaError_t launch_attn_bf16_d64(const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
+                                 float* acc_lse, float scale, cudaStream_t stream);
+int d64_rows_per_item();
+int d64_kv_box_rows();
 
 // D = 128 runs on CTA pairs (cta_group::2, 512 query rows per item; K maps with 64-row boxes);
-// D = 64 on single CTAs (256 rows per item).  Callers size work items with attn_rows_per_item
-// and build the Q / K / V maps with attn_box_rows(D, 0 / 1 / 2).
+// D = 64 on the two-tile kernel above; -DCQS_D64_DBS routes it to the double-buffered-S
+// kernel (attn_bf16_sm100_d64.cu: parity-green, measured 680 vs 695 TFLOP/s on C2-d64).
+// Callers size work items with attn_rows_per_item and build the Q / K / V maps with
+// attn_box_rows(D, 0 / 1 / 2).
+int attn_rows_per_item(int D) {
 #ifndef CQS_ONE_CTA_D128
-int attn_rows_per_item(int D) { return D == 128 ? 512 : 256; }
-int attn_box_rows(int D, int which) { return (D == 128 && which == 1) ? 64 : 128; }
-#else
-int attn_rows_per_item(int) { return 256; }
-int attn_box_rows(int, int) { return 128; }
+  if (D == 128) return 512;
 #endif
+#ifdef CQS_D64_DBS
+  if (D == 64) return d64_rows_per_item();
+#endif
+  return 256;
+}
+int attn_box_rows(int D, int which) {
+#ifndef CQS_ONE_CTA_D128
+  if (D == 128 && which == 1) return 64;
+#endif
+#ifdef CQS_D64_DBS
+  if (D == 64 && which != 0) return d64_kv_box_rows();
+#endif
+  return 128;
+}
 
 cudaError_t launch_attn_bf16(int D, const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
                              float* acc_lse, float scale, cudaStream_t stream) {
@@ -474,7 +524,11 @@ cudaError_t launch_attn_bf16(int D, const CUtensorMap* maps, const TaskParams& t
 #else
   if (D == 128) return launch_bf16_impl<128>(maps, tp, acc_o, acc_lse, scale, stream);
 #endif
+#ifdef CQS_D64_DBS
+  if (D == 64) return launch_attn_bf16_d64(maps, tp, acc_o, acc_lse, scale, stream);
+#else
   if (D == 64) return launch_bf16_impl<64>(maps, tp, acc_o, acc_lse, scale, stream);
+#endif
   return cudaErrorInvalidValue;
 }
 

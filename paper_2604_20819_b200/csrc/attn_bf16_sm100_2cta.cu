@@ -90,6 +90,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
   const uint32_t kmask = tp.kept[a];
   int n_kv = 0;
   for (uint32_t m = kmask; m; m &= m - 1) n_kv += (tp.seg_len[__ffs(m) - 1] + kBN - 1) / kBN;
+  const int kv0 = kv_start(item, n_kv);
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(q_full, 1);
@@ -134,8 +135,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         return true;
       };
       KvCursor ck, cv;
-      ck.init(&tp, kmask);
-      cv.init(&tp, kmask);
+      ck.init(&tp, kmask, kv0);
+      cv.init(&tp, kmask, kv0);
       auto load_k = [&]() {   // keys [64 rank, 64 rank + 64) of the tile, both 64-col boxes
         const int s = it % kStages;
         if (stage_wait(s))
@@ -256,7 +257,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
       long long dc[12] = {};
 #endif
       KvCursor cur;
-      cur.init(&tp, kmask);
+      cur.init(&tp, kmask, kv0);
       for (int j = 0; j < n_kv; ++j) {
         const int valid = cur.valid();
         cur.next();
