@@ -1,7 +1,7 @@
 """BASELINE config 2: N = 1,000,000 tokens, 32 heads, D = 128, bf16, Q/K/V (and O, lse) in pinned
 host memory, 16 GiB device budget -> the planner picks two CQS levels (49 tasks).  Times one full
 streamed forward through the public C ABI and reports throughput, peak device memory against the
-budget, H2D traffic and sampled-row parity against the fp64 oracle.
+budget, H2D traffic and sampled-row parity against an fp64 sampled-row reference (tools/_rowref.py).
 
     python tools/c3_bench.py > profiles/r01_c3_streamed.json
 """
@@ -19,7 +19,7 @@ def main():
     import torch
     import cqs_synth
     import paper_2604_20819_b200 as cqs
-    from oracle import cqs_oracle as O
+    from tools import _rowref as R
 
     B, H, N, D = 1, 32, 1_000_000, 128
     budget = 16 << 30
@@ -75,7 +75,7 @@ def main():
     errs, lerrs = [], []
     for h in rng.choice(H, 2, replace=False):
         rows = np.sort(rng.choice(N, 8, replace=False))
-        Oref, lref = O.dense_attention_rows(q[0, h].double().numpy(), k[0, h].double().numpy(),
+        Oref, lref = R.rows_forward(q[0, h].double().numpy(), k[0, h].double().numpy(),
                                             v[0, h].double().numpy(), rows, block=1 << 18)
         errs.append(float(np.abs(out[0, h, rows].double().numpy() - Oref).max()))
         lerrs.append(float(np.abs(lse[0, h, rows].double().numpy() - lref).max()))

@@ -6,7 +6,7 @@ pinned host).  Measured: t7 and the useful FLOP rate.  Extrapolated two ways:
   paper   : t_1B = t7 * 7^(itr-1)                         (Table 1 "Est. t_fwd")
   by work : t_1B = 4 N^2 D / (measured useful FLOP rate)  (at itr=6 ~40% of leaves are
             empty and kept area shrinks by (7/9)^itr, so counting leaves over-estimates)
-Parity: sampled output rows against the fp64 oracle over all N' keys.
+Parity: sampled output rows against an fp64 sampled-row reference (tools/_rowref.py) over all N' keys.
 
     python tools/c5_scaled.py [--itr 6] [--rows 8] > profiles/r01_c5_scaled.json
 """
@@ -31,7 +31,7 @@ def main():
     import torch
     import cqs_synth
     import paper_2604_20819_b200 as cqs
-    from oracle import cqs_oracle as O
+    from tools import _rowref as R
 
     N_full, H, D = 10 ** 9, 1, 64
     Np = int(round(N_full * (3 / 7) ** (args.itr - 1)))
@@ -69,7 +69,7 @@ def main():
     rows = np.sort(rng.choice(Np, args.rows, replace=False))
     kk = k[0, 0].double().numpy()
     vv = v[0, 0].double().numpy()
-    Oref, lref = O.dense_attention_rows(q[0, 0].double().numpy(), kk, vv, rows, block=1 << 20)
+    Oref, lref = R.rows_forward(q[0, 0].double().numpy(), kk, vv, rows, block=1 << 20)
     o = out[0, 0, rows].double().numpy()
     l_ = lse[0, 0, rows].double().numpy()
     res = {
@@ -102,7 +102,7 @@ def backward(args, q, k, v, out, lse, Np, H, D, N_full, seed):
     import torch
     import cqs_synth
     import paper_2604_20819_b200 as cqs
-    from oracle import cqs_oracle as O
+    from tools import _rowref as R
     budget = int(args.budget_gib * (1 << 30))
     do = cqs_synth.torch_tensor((1, H, Np, D), seed, "do", torch.bfloat16, "cuda").cpu().pin_memory()
     torch.cuda.empty_cache()
@@ -127,7 +127,7 @@ def backward(args, q, k, v, out, lse, Np, H, D, N_full, seed):
     rng = np.random.default_rng(6)
     rows = np.sort(rng.choice(Np, 4, replace=False))
     f = lambda t: t[0, 0].double().numpy()
-    ref = O.dense_dq_rows(f(q), f(k), f(v), f(do), rows, block=1 << 20)
+    ref = R.rows_dq(f(q), f(k), f(v), f(do), rows, block=1 << 20)
     got = dq[0, 0, rows].double().numpy()
     rel = np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)
     return {"t7_bwd_s": t7, "useful_tflops_algorithmic": rate / 1e12, "mode": "streamed",
