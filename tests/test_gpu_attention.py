@@ -210,3 +210,18 @@ def test_bf16_mixed_level_interest_sets(levels, N, depth):
     cqs.cqs_attention_forward(p, q, k, v, out, lse, 0.0, 0, ws, None)
     torch.cuda.synchronize()
     check_bf16(out, lse, *ref_dense(q, k, v))
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("N,depth", [(1, 0), (2, 0), (7, 1), (127, 0), (128, 0), (129, 0),
+                                     (255, 1), (256, 1), (257, 1), (511, 0), (512, 0), (513, 0),
+                                     (1025, 1), (343, 3)])
+def test_bf16_tile_boundaries(N, depth, D):
+    """Ragged sizes around the kernels' tile and work-item edges (128-row tiles; 256-row items at
+    D=64, 512-row CTA-pair items at D=128, where one CTA of the pair or one tile may hold no row
+    of the segment), one to three heads, single-token chunks at depth 1/3."""
+    H = 1 + N % 3
+    q, k, v = gen(1, H, N, D, 900 + N + D, bf16=True)
+    out, lse = cqs.attention(q, k, v, depth=depth)
+    torch.cuda.synchronize()
+    check_bf16(out, lse, *ref_dense(q, k, v))

@@ -4,6 +4,7 @@ streamed forward through the public C ABI and reports throughput, peak device me
 budget, H2D traffic and sampled-row parity against an fp64 sampled-row reference (tools/_rowref.py).
 
     python tools/c3_bench.py > profiles/r01_c3_streamed.json
+    python tools/c3_bench.py --N 16777216 --H 1 --D 64 --budget-gib 1 --runs 1   # deep tree (NEXT-4)
 """
 import json
 import os
@@ -21,8 +22,16 @@ def main():
     import paper_2604_20819_b200 as cqs
     from tools import _rowref as R
 
-    B, H, N, D = 1, 32, 1_000_000, 128
-    budget = 16 << 30
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--N", type=int, default=1_000_000)
+    ap.add_argument("--H", type=int, default=32)
+    ap.add_argument("--D", type=int, default=128)
+    ap.add_argument("--budget-gib", type=float, default=16.0)
+    ap.add_argument("--runs", type=int, default=2)
+    args = ap.parse_args()
+    B, H, N, D = 1, args.H, args.N, args.D
+    budget = int(args.budget_gib * (1 << 30))
     seed = 20260419
     q, k, v = (cqs_synth.torch_tensor((B, H, N, D), seed, nm, torch.bfloat16, "cuda").cpu()
                .pin_memory() for nm in ("q", "k", "v"))
@@ -38,13 +47,15 @@ def main():
     hws = torch.empty(max(host, 256), dtype=torch.uint8).pin_memory() if host else None
     out = torch.empty((B, H, N, D), dtype=torch.bfloat16).pin_memory()
     lse = torch.empty((B, H, N), dtype=torch.float32).pin_memory()
-    cqs.attention(*(t[:, :2, :8192].cuda() for t in (q, k, v)), depth=1)   # warm-up
+    cqs.attention(*(t[:, :min(2, H), :8192].cuda() for t in (q, k, v)), depth=1)   # warm-up
     torch.cuda.synchronize()
-    res = {"config": "C3: N=1e6, H=32, D=128, bf16, QKV/O in pinned host memory, 16 GiB budget",
+    res = {"config": "%sN=%d, H=%d, D=%d, bf16, QKV/O in pinned host memory, %.4g GiB budget" % (
+               "C3: " if (N, H, D, args.budget_gib) == (1_000_000, 32, 128, 16.0) else "", N, H, D,
+               args.budget_gib),
            "depth": info.depth, "tasks": info.n_tasks, "acc_depth": info.acc_depth,
            "stage_buffers": info.n_stage_buffers, "budget_bytes": budget,
            "predicted_peak_bytes": info.predicted_peak_bytes, "runs": []}
-    for _ in range(2):
+    for _ in range(args.runs):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         st = cqs.cqs_attention_forward(plan, q, k, v, out, lse, 0.0, budget, ws, hws, stats=True)
@@ -73,7 +84,7 @@ def main():
     res["peak_within_budget"] = res["measured_peak_dev_bytes"] <= budget + 512
     rng = np.random.default_rng(9)
     errs, lerrs = [], []
-    for h in rng.choice(H, 2, replace=False):
+    for h in rng.choice(H, min(2, H), replace=False):
         rows = np.sort(rng.choice(N, 8, replace=False))
         Oref, lref = R.rows_forward(q[0, h].double().numpy(), k[0, h].double().numpy(),
                                             v[0, h].double().numpy(), rows, block=1 << 18)
