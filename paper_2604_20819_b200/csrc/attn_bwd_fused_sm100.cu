@@ -1,6 +1,7 @@
 // EXPERIMENT (built into libcqs, selected only by -DCQS_BWD_FUSED builds; the default backward is
-// the dK/dV + dQ kernel pair in attn_bwd_sm100.cu, which measured 23% faster — see
-// profiles/r01_notes.md "Backward").
+// the dK/dV + dQ kernel pair in attn_bwd_sm100.cu, which measured 22% faster: 889 vs 1139 ms per
+// C2 step with the vectorised dQ drain below, 1427 ms with one red.f32 per element
+// (-DCQS_BWD_RED_SCALAR) — see profiles/r01_notes.md "Backward").
 // Fused per-task CQS attention backward for D = 128 (sm_100a tcgen05 / TMEM / TMA): one kernel
 // computes dK, dV AND dQ of a task (Algorithm 2), so S and dP are computed
 // once per kept block (10·D FLOP per pair instead of the two-kernel split's 14·D).
@@ -16,8 +17,8 @@
 //                              N = 64 queries) into the TMEM columns of dP^T_h, which the EW pass
 //                              has already consumed
 //   drain (warps 8-11, thread = d = TMEM lane): tcgen05.ld the 64 columns, release the columns,
-//       red.global.add.f32 alpha·dQ^T into the fp32 dQ accumulator (coalesced: a warp instruction
-//       covers 32 consecutive d of one query row = 128 B)
+//       4x4 shuffle transposes within lane quads, then red.global.add.v4.f32 alpha·dQ into the fp32
+//       dQ accumulator (a warp instruction covers 4 query rows x 32 consecutive d = 4 x 128 B)
 // TMEM (512 columns): S^T | dP^T (= dQ^T after EW) | dV | dK.
 // Shared memory: K, V (64 KB) + 2 stages x (Q, dO) (128 KB) + sdS[2] (32 KB) + lse/Delta (2 KB):
 // 226 KB, so the dynamic smem base must already be 1024-byte aligned (checked; traps otherwise).
@@ -51,6 +52,11 @@ __device__ __forceinline__ uint64_t kstep_k(int ks) {   // K-major SW128 tile of
 
 __device__ __forceinline__ void red_add_f32(float* p, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -341,11 +347,38 @@ __global__ void __launch_bounds__(fused::kThreads, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&dq_empty[h]);
         const int nv = min(64, valid_q - h * 64);
-        float* base = dq_acc + (q_dst + h * 64) * tp.BH * D + int64_t(bh) * D + d;
         const int64_t row_stride = int64_t(tp.BH) * D;
+#ifdef CQS_BWD_RED_SCALAR
+        float* base = dq_acc + (q_dst + h * 64) * tp.BH * D + int64_t(bh) * D + d;
 #pragma unroll
         for (int j = 0; j < 64; ++j)
           if (j < nv) red_add_f32(base + j * row_stride, scale * __uint_as_float(v[j]));
+#else
+        // 4x4 transposes across lane quads (lane 4g+i holds d = 32 sub + 4g + i): afterwards lane
+        // 4g+i holds, for query 4qb+i, the four consecutive d = 32 sub + 4g .. +3, so one
+        // red.global.add.v4.f32 per (thread, 4 queries) and a warp instruction covers 4 query rows
+        // x 128 B (4x fewer reduction instructions than one f32 per element)
+        const int i4 = lane & 3;
+        float* base = dq_acc + (q_dst + h * 64 + i4) * row_stride + int64_t(bh) * D + sub * 32 +
+                      (lane & ~3);
+#pragma unroll
+        for (int qb = 0; qb < 16; ++qb) {
+          float a0 = __uint_as_float(v[4 * qb]), a1 = __uint_as_float(v[4 * qb + 1]);
+          float a2 = __uint_as_float(v[4 * qb + 2]), a3 = __uint_as_float(v[4 * qb + 3]);
+          const bool lo2 = (i4 & 2) == 0, even = (i4 & 1) == 0;
+          const float t0 = __shfl_xor_sync(0xffffffffu, lo2 ? a2 : a0, 2);
+          const float t1 = __shfl_xor_sync(0xffffffffu, lo2 ? a3 : a1, 2);
+          if (lo2) a2 = t0, a3 = t1;
+          else a0 = t0, a1 = t1;
+          const float u0 = __shfl_xor_sync(0xffffffffu, even ? a1 : a0, 1);
+          const float u1 = __shfl_xor_sync(0xffffffffu, even ? a3 : a2, 1);
+          if (even) a1 = u0, a3 = u1;
+          else a0 = u0, a2 = u1;
+          if (4 * qb + i4 < nv)
+            red_add_v4(base + int64_t(4 * qb) * row_stride, scale * a0, scale * a1, scale * a2,
+                       scale * a3);
+        }
+#endif
       }
     }
   }
