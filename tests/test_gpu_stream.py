@@ -82,8 +82,16 @@ def test_c3_streamed_16gib_sampled():
     out, lse, info, st, peak = run_streamed(q, k, v, budget)
     assert info.depth == 2 and peak <= budget + 512
     rng = np.random.default_rng(2)
-    for h in rng.choice(H, 2, replace=False):
-        rows = np.sort(rng.choice(N, 16, replace=False))
+    # 4 heads x 64 rows: random rows plus the first / last token and both sides of every level-1
+    # and level-2 chunk boundary (BalancedChunkLayout, R1)
+    edges = []
+    for c in (7, 49):
+        base, rem = divmod(N, c)
+        b = np.cumsum([base + (i < rem) for i in range(c)])[:-1]
+        edges += list(b - 1) + list(b)
+    for h in rng.choice(H, 4, replace=False):
+        pick = rng.choice(edges, 24, replace=False)
+        rows = np.unique(np.concatenate([[0, N - 1], pick, rng.choice(N, 38, replace=False)]))
         Oref, lref = O.dense_attention_rows(q[0, h].double().numpy(), k[0, h].double().numpy(),
                                             v[0, h].double().numpy(), rows, block=65536)
         o = out[0, h, rows].double().numpy()
