@@ -40,6 +40,13 @@ __device__ unsigned long long g_cqs_dbg1[16];
 #define DBG1_ADD(i, x) ((void)0)
 #endif
 constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
+// setmaxnreg split (see the register note in the kernel): 4 warps at LO, 8 softmax warps at HI
+// (56 / 224: no spills; measured +3.9% over 72 / 216 at D = 64: 725 vs 697 TFLOP/s, 3 runs each)
+#ifndef CQS_ONE_REG_LO
+#define CQS_ONE_REG_LO 56
+#define CQS_ONE_REG_HI 224
+#endif
+static_assert(128 * (168 - CQS_ONE_REG_LO) == 256 * (CQS_ONE_REG_HI - 168), "register split");
 // column pairs (i mod 8) whose exp2 runs on the FMA pipe instead of MUFU
 // (measured on B200, C2 shape, fused exp loop: MUFU-only is fastest at both head dims — D=64:
 // 750 TFLOP/s MUFU-only vs 716 at 1/4 of the pairs emulated, 658 at 1/2, 534 at 3/4; D=128 is
@@ -143,11 +150,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // register split (launch: 384 x 168): the 4 non-math warps give back 128 x (168-72) = 12288
-  // registers, exactly what the 8 softmax warps take (256 x (216-168)); .inc blocks forever if
-  // the pool is short, so the two numbers must balance.
+  // register split (launch: 384 x 168): the 4 non-math warps give back 128 x (168-LO) registers,
+  // exactly what the 8 softmax warps take (256 x (HI-168)); .inc blocks forever if the pool is
+  // short, so the two numbers must balance (static_assert above).
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(CQS_ONE_REG_LO) : "memory");
   if (warp == 0) {
     // ================= TMA producer =================
     if (lane == 0) {
@@ -280,7 +287,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
   }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CQS_ONE_REG_HI) : "memory");
     // ================= softmax / correction / epilogue =================
     const int t = (warp - 4) >> 2;
     if (t == 0 || two) {

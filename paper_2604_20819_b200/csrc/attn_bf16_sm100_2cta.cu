@@ -35,6 +35,14 @@ constexpr int kStages = 8;
 constexpr int kSmemBytes = 2 * kQBytes + kStages * kStageBytes + 1024 + 512;
 constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 384;
 constexpr float kRescaleThreshold = 8.0f;
+// setmaxnreg split of the 384 x 168 launch registers: 4 producer / MMA / allocator warps at LO,
+// 8 softmax warps at HI, with 128 (168 - LO) = 256 (HI - 168) (an unbalanced .inc blocks forever)
+// (56 / 224: no spills; measured +1.7% over 72 / 216 on C2: 1129 vs 1110 TFLOP/s, 3 runs each)
+#ifndef CQS_PAIR_REG_LO
+#define CQS_PAIR_REG_LO 56
+#define CQS_PAIR_REG_HI 224
+#endif
+static_assert(128 * (168 - CQS_PAIR_REG_LO) == 256 * (CQS_PAIR_REG_HI - 168), "register split");
 // Split S: S_t(j+1) is issued as two N = 64 halves.  Half 0 (keys 0-31 of CTA 0's K rows and
 // 64-95 of CTA 1's) lands in columns [64, 128) of the tile's S region, which the softmax has
 // already read into registers (it signals s_loaded right after its tcgen05.ld), so it can run
@@ -128,7 +136,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(CQS_PAIR_REG_LO) : "memory");
     if (warp == 0 && lane == 0) {
       // ================= TMA producer (both CTAs) =================
       ptx::tma_prefetch_desc(&tmQ);
@@ -288,7 +296,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
 #endif
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CQS_PAIR_REG_HI) : "memory");
     // ================= softmax / correction / epilogue (both CTAs) =================
     const int t = (warp - 4) >> 2;
     if (t == 0 || two) {
