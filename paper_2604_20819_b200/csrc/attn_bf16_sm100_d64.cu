@@ -145,7 +145,7 @@ __global__ void CQS_D64_CLUSTER __launch_bounds__(d64::kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
     if (warp == 0 && lane == 0) {
       // ================= TMA producer: Q, then K_0, K_1, (V_j, K_{j+2})... =================
       ptx::tma_prefetch_desc(&tmQ);
@@ -254,7 +254,7 @@ __global__ void CQS_D64_CLUSTER __launch_bounds__(d64::kThreads, 1)
 #endif
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
     // ================= softmax (key half h of rows r), correction, epilogue =================
     const int h = (warp - 4) >> 2;
     const int sub = warp & 3;
