@@ -42,6 +42,24 @@ struct BwdCfg {
   static constexpr int kSmemKV = 2 * kTile + kStages * kStageKV + 1024 + 256;
   static constexpr int kSmemQ = 2 * kTile + kStages * 2 * kTile + 1024 + 256;
   static constexpr uint32_t kColS = 0, kColP = 128, kColA0 = 256, kColA1 = 256 + D;
+  // dQ kernel: the CTA's Q and dO tiles (the A operands of S = Q K^T and dP = dO V^T, fixed for the
+  // whole CTA) live in the TMEM columns after the dQ accumulator, so those MMAs read only K / V
+  // from shared memory (an SS MMA at M = 128, N = 64 needs 192 B/clk of SMEM, over the 128 B/clk
+  // available; with A in TMEM it needs 64)
+  static constexpr uint32_t kColQ = 256 + D, kColdO = 256 + D + D / 2;
+#ifdef CQS_BWD_DQ_SMEM_A
+  static constexpr bool kQdOInTmem = false;
+#else
+  static constexpr bool kQdOInTmem = true;
+#endif
+  // dK/dV kernel at D = 64: the CTA's K and V tiles (A of S^T = K Q^T, dP^T = V dO^T) in TMEM after
+  // the dK accumulator; at D = 128 the four 128-column regions use all 512 columns
+  static constexpr uint32_t kColKT = 256 + 2 * D, kColVT = 256 + 2 * D + D / 2;
+#ifdef CQS_BWD_DKDV_SMEM_A
+  static constexpr bool kKVInTmem = false;
+#else
+  static constexpr bool kKVInTmem = D == 64;
+#endif
 };
 
 // descriptor offset of the 16-wide K step `ks` in a K-major SW128 tile of 128 rows
@@ -145,7 +163,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* s_full = qd_empty + C::kStages;       // 2 (halves)
   uint64_t* p_full = s_full + 2;                  // 2
   uint64_t* acc_done = p_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
+  uint64_t* kv_tm = acc_done + 1;                 // K / V copied into TMEM (kKVInTmem, 4 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_tm + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int bh, b, k_off;
@@ -166,6 +185,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ptx::mbar_init(&p_full[h], 4);
     }
     ptx::mbar_init(acc_done, 1);
+    ptx::mbar_init(kv_tm, 4);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
@@ -224,13 +244,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint64_t st = uint64_t((i % C::kStages) * C::kStageKV) >> 4;
       const uint64_t hq = uint64_t(h * 64 * 128) >> 4;   // query rows h*64.. of the tile
 #pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks)
-        ptx::mma_ss_elect(tmem + C::kColS + h * 64, dK + kstep_off(ks),
-                          dSt + st + hq + kstep_off(ks), idesc_s, ks > 0);
+      for (int ks = 0; ks < D / 16; ++ks) {
+        if constexpr (C::kKVInTmem)
+          ptx::mma_ts_elect(tmem + C::kColS + h * 64, tmem + C::kColKT + ks * 8,
+                            dSt + st + hq + kstep_off(ks), idesc_s, ks > 0);
+        else
+          ptx::mma_ss_elect(tmem + C::kColS + h * 64, dK + kstep_off(ks),
+                            dSt + st + hq + kstep_off(ks), idesc_s, ks > 0);
+      }
 #pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks)
-        ptx::mma_ss_elect(tmem + C::kColP + h * 64, dV + kstep_off(ks),
-                          dSt + st + (C::kTile >> 4) + hq + kstep_off(ks), idesc_s, ks > 0);
+      for (int ks = 0; ks < D / 16; ++ks) {
+        if constexpr (C::kKVInTmem)
+          ptx::mma_ts_elect(tmem + C::kColP + h * 64, tmem + C::kColVT + ks * 8,
+                            dSt + st + (C::kTile >> 4) + hq + kstep_off(ks), idesc_s, ks > 0);
+        else
+          ptx::mma_ss_elect(tmem + C::kColP + h * 64, dV + kstep_off(ks),
+                            dSt + st + (C::kTile >> 4) + hq + kstep_off(ks), idesc_s, ks > 0);
+      }
       ptx::mma_commit_elect(&s_full[h]);
     };
     auto issue_G = [&](int i, int h) {
@@ -245,7 +275,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                           idesc_g, acc);                                        // dK += dS^T Q
       }
     };
-    ptx::mbar_wait(kv_full, 0);
+    ptx::mbar_wait(C::kKVInTmem ? kv_tm : kv_full, 0);
     ptx::mbar_wait(&qd_full[0], 0);
     ptx::tc_fence_after();
     issue_SdP(0, 0);
@@ -274,6 +304,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t lane_base = uint32_t(sub * 32) << 16;
     const uint32_t tS = tmem + lane_base + C::kColS, tP = tmem + lane_base + C::kColP;
     const uint64_t sc2 = ptx::f2(scale_log2, scale_log2);
+    if constexpr (C::kKVInTmem) {
+      // key row r of K and V (one SW128 box at D = 64) -> TMEM columns kColKT / kColVT
+      ptx::mbar_wait(kv_full, 0);
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const uint8_t* base = (g ? sV : sK) + r * 128;
+        uint32_t kv[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 u = *reinterpret_cast<const uint4*>(base + ((c ^ (r & 7)) << 4));
+          kv[4 * c + 0] = u.x, kv[4 * c + 1] = u.y, kv[4 * c + 2] = u.z, kv[4 * c + 3] = u.w;
+        }
+        ptx::tmem_st32(tmem + lane_base + (g ? C::kColVT : C::kColKT), kv);
+      }
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(kv_tm);
+    }
     KvCursor cq;
     cq.init(&tp, qmask);
     for (int i = 0; i < n_q; ++i) {
@@ -341,7 +390,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* s_full = kv_empty + C::kStages;
   uint64_t* p_full = s_full + 2;
   uint64_t* acc_done = p_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
+  uint64_t* q_tm = acc_done + 1;                  // Q / dO copied into TMEM (4 EW warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_tm + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int bh, a, q_off;
@@ -362,6 +412,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       ptx::mbar_init(&p_full[h], 4);
     }
     ptx::mbar_init(acc_done, 1);
+    ptx::mbar_init(q_tm, 4);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(tmem_slot, 512);
@@ -407,13 +458,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint64_t st = uint64_t((j % C::kStages) * 2 * C::kTile) >> 4;
       const uint64_t hk = uint64_t(h * 64 * 128) >> 4;
 #pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks)
-        ptx::mma_ss_elect(tmem + C::kColS + h * 64, dQd + kstep_off(ks),
-                          dSt + st + hk + kstep_off(ks), idesc_s, ks > 0);
+      for (int ks = 0; ks < D / 16; ++ks) {
+        if constexpr (C::kQdOInTmem)
+          ptx::mma_ts_elect(tmem + C::kColS + h * 64, tmem + C::kColQ + ks * 8,
+                            dSt + st + hk + kstep_off(ks), idesc_s, ks > 0);
+        else
+          ptx::mma_ss_elect(tmem + C::kColS + h * 64, dQd + kstep_off(ks),
+                            dSt + st + hk + kstep_off(ks), idesc_s, ks > 0);
+      }
 #pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks)
-        ptx::mma_ss_elect(tmem + C::kColP + h * 64, ddO + kstep_off(ks),
-                          dSt + st + (C::kTile >> 4) + hk + kstep_off(ks), idesc_s, ks > 0);
+      for (int ks = 0; ks < D / 16; ++ks) {
+        if constexpr (C::kQdOInTmem)
+          ptx::mma_ts_elect(tmem + C::kColP + h * 64, tmem + C::kColdO + ks * 8,
+                            dSt + st + (C::kTile >> 4) + hk + kstep_off(ks), idesc_s, ks > 0);
+        else
+          ptx::mma_ss_elect(tmem + C::kColP + h * 64, ddO + kstep_off(ks),
+                            dSt + st + (C::kTile >> 4) + hk + kstep_off(ks), idesc_s, ks > 0);
+      }
       ptx::mma_commit_elect(&s_full[h]);
     };
     auto issue_G = [&](int j, int h) {
@@ -425,7 +486,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                           idesc_g, (j | h | kk) != 0);                         // dQ += dS K
       }
     };
-    ptx::mbar_wait(qd_full, 0);
+    ptx::mbar_wait(C::kQdOInTmem ? q_tm : qd_full, 0);
     ptx::mbar_wait(&kv_full[0], 0);
     ptx::tc_fence_after();
     issue_SdP(0, 0);
@@ -461,6 +522,30 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       dl = ld[(int64_t(bh) * 2 + 1) * ld_pitch + q_row];
     }
     const uint64_t nl2 = ptx::f2(nl, nl), dl2 = ptx::f2(dl, dl);
+    if constexpr (C::kQdOInTmem) {
+      // row r of the Q and dO tiles (SW128 boxes of 64 columns: 16-byte chunk c of row r sits at
+      // chunk c ^ (r & 7)) -> packed bf16 pairs -> TMEM columns kColQ / kColdO (packed like P)
+      ptx::mbar_wait(qd_full, 0);
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const uint8_t* base = (g ? sdO : sQ) + r * 128;
+#pragma unroll
+        for (int bx = 0; bx < C::kBoxes; ++bx) {
+          uint32_t qv[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 u =
+                *reinterpret_cast<const uint4*>(base + bx * 128 * 128 + ((c ^ (r & 7)) << 4));
+            qv[4 * c + 0] = u.x, qv[4 * c + 1] = u.y, qv[4 * c + 2] = u.z, qv[4 * c + 3] = u.w;
+          }
+          ptx::tmem_st32(tmem + lane_base + (g ? C::kColdO : C::kColQ) + bx * 32, qv);
+        }
+      }
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(q_tm);
+    }
     KvCursor ck;
     ck.init(&tp, kmask);
     for (int j = 0; j < n_kv; ++j) {
