@@ -30,7 +30,21 @@
 
 namespace cqs {
 
-constexpr int kBwdThreads = 256;
+// Elementwise (EW) pass on 8 warps: warps w and w + 4 share a TMEM lane quarter (rows) and split
+// each 64-column half-tile into 32-column chunks, so two warps per SM sub-partition feed the MUFU
+// (one warp alone reaches ~79% of its rate, two ~89%: tools/softmax_bench.cu).  Each chunk's P / dS
+// (bf16 pairs) is written at the start of its own 32 source columns, so the two warps never write
+// columns the other still has to read; the MMAs read the A operand at ew_acol(kk).
+#ifdef CQS_BWD_EW4
+constexpr bool kEW8 = false;
+#else
+constexpr bool kEW8 = true;
+#endif
+constexpr int kBwdThreads = kEW8 ? 384 : 256;
+__device__ __forceinline__ constexpr uint32_t ew_ocol(int c) { return kEW8 ? c * 32 : c * 16; }
+__device__ __forceinline__ constexpr uint32_t ew_acol(int kk) {
+  return kEW8 ? (kk >> 1) * 32 + (kk & 1) * 8 : kk * 8;
+}
 
 template <int D>
 struct BwdCfg {
@@ -69,7 +83,7 @@ __device__ __forceinline__ uint64_t kstep_off(int ks) {
 
 // One elementwise pass over 32 columns of S / dP held in TMEM (fp32 at tS / tP), writing P and dS
 // as packed bf16 pairs to the 16 columns at oS / oP (chunk c of a 64-column half lands on columns
-// c*16.. of the half, the K-major TMEM A operand of the next MMA).  nl2/dl2: per-column
+// ew_ocol(c).. of the half, the K-major TMEM A operand of the next MMA, read at ew_acol(kk)).  nl2/dl2: per-column
 // (-lse*log2e, Delta) pairs; valid: columns >= valid are masked to zero.
 template <bool kWriteP>
 __device__ __forceinline__ void bwd_ew_chunk(uint32_t tS, uint32_t tP, uint32_t oS, uint32_t oP,
@@ -182,7 +196,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     for (int h = 0; h < 2; ++h) {
       ptx::mbar_init(&s_full[h], 1);
-      ptx::mbar_init(&p_full[h], 4);
+      ptx::mbar_init(&p_full[h], kEW8 ? 8 : 4);
     }
     ptx::mbar_init(acc_done, 1);
     ptx::mbar_init(kv_tm, 4);
@@ -269,10 +283,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int kk = 0; kk < 4; ++kk) {
         const uint64_t qr = uint64_t((h * 64 + kk * 16) * 128) >> 4;
         const uint32_t acc = (i | h | kk) != 0;
-        ptx::mma_ts_elect(tmem + C::kColA0, tmem + C::kColS + h * 64 + kk * 8,
+        ptx::mma_ts_elect(tmem + C::kColA0, tmem + C::kColS + h * 64 + ew_acol(kk),
                           dStMN + st + (C::kTile >> 4) + qr, idesc_g, acc);   // dV += P^T dO
-        ptx::mma_ts_elect(tmem + C::kColA1, tmem + C::kColP + h * 64 + kk * 8, dStMN + st + qr,
-                          idesc_g, acc);                                        // dK += dS^T Q
+        ptx::mma_ts_elect(tmem + C::kColA1, tmem + C::kColP + h * 64 + ew_acol(kk),
+                          dStMN + st + qr, idesc_g, acc);                       // dK += dS^T Q
       }
     };
     ptx::mbar_wait(C::kKVInTmem ? kv_tm : kv_full, 0);
@@ -300,11 +314,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     ptx::mma_commit_elect(acc_done);
   } else if (warp >= 4) {
     const int sub = warp & 3;
+    const int cw = (warp - 4) >> 2;                  // kEW8: this warp's 32-column chunk
     const int r = sub * 32 + lane;
     const uint32_t lane_base = uint32_t(sub * 32) << 16;
     const uint32_t tS = tmem + lane_base + C::kColS, tP = tmem + lane_base + C::kColP;
     const uint64_t sc2 = ptx::f2(scale_log2, scale_log2);
-    if constexpr (C::kKVInTmem) {
+    if (C::kKVInTmem && cw == 0) {
       // key row r of K and V (one SW128 box at D = 64) -> TMEM columns kColKT / kColVT
       ptx::mbar_wait(kv_full, 0);
 #pragma unroll
@@ -336,10 +351,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::mbar_wait(&s_full[h], i & 1);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        for (int cc = 0; cc < (kEW8 ? 1 : 2); ++cc) {
+          const int c = kEW8 ? cw : cc;
           const int q0 = h * 64 + c * 32;
-          bwd_ew_chunk<true>(tS + h * 64 + c * 32, tP + h * 64 + c * 32, tS + h * 64 + c * 16,
-                             tP + h * 64 + c * 16, q0, valid_q, sc2,
+          bwd_ew_chunk<true>(tS + h * 64 + c * 32, tP + h * 64 + c * 32, tS + h * 64 + ew_ocol(c),
+                             tP + h * 64 + ew_ocol(c), q0, valid_q, sc2,
                              reinterpret_cast<const uint64_t*>(sLD + q0),
                              reinterpret_cast<const uint64_t*>(sLD + 128 + q0), true);
         }
@@ -353,8 +369,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     ptx::tc_fence_after();
     const bool live = r < min(128, tp.seg_len[b] - k_off);
     const int64_t idx = int64_t(tp.seg_dst[b] + k_off + r) * tp.BH + bh;
-    bwd_store_acc<D>(tmem + lane_base + C::kColA0, dv_acc + idx * D, 1.f, live);
-    bwd_store_acc<D>(tmem + lane_base + C::kColA1, dk_acc + idx * D, scale, live);
+    if (!kEW8 || cw == 0) bwd_store_acc<D>(tmem + lane_base + C::kColA0, dv_acc + idx * D, 1.f, live);
+    if (!kEW8 || cw == 1) bwd_store_acc<D>(tmem + lane_base + C::kColA1, dk_acc + idx * D, scale, live);
   }
 
   ptx::tc_fence_before();
@@ -409,7 +425,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     for (int h = 0; h < 2; ++h) {
       ptx::mbar_init(&s_full[h], 1);
-      ptx::mbar_init(&p_full[h], 4);
+      ptx::mbar_init(&p_full[h], kEW8 ? 8 : 4);
     }
     ptx::mbar_init(acc_done, 1);
     ptx::mbar_init(q_tm, 4);
@@ -482,8 +498,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const uint64_t kr = uint64_t((h * 64 + kk * 16) * 128) >> 4;
-        ptx::mma_ts_elect(tmem + C::kColA0, tmem + C::kColP + h * 64 + kk * 8, dStMN + st + kr,
-                          idesc_g, (j | h | kk) != 0);                         // dQ += dS K
+        ptx::mma_ts_elect(tmem + C::kColA0, tmem + C::kColP + h * 64 + ew_acol(kk),
+                          dStMN + st + kr, idesc_g, (j | h | kk) != 0);        // dQ += dS K
       }
     };
     ptx::mbar_wait(C::kQdOInTmem ? q_tm : qd_full, 0);
@@ -511,6 +527,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     ptx::mma_commit_elect(acc_done);
   } else if (warp >= 4) {
     const int sub = warp & 3;
+    const int cw = (warp - 4) >> 2;                  // kEW8: this warp's 32-column chunk
     const int r = sub * 32 + lane;
     const uint32_t lane_base = uint32_t(sub * 32) << 16;
     const uint32_t tS = tmem + lane_base + C::kColS, tP = tmem + lane_base + C::kColP;
@@ -522,7 +539,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       dl = ld[(int64_t(bh) * 2 + 1) * ld_pitch + q_row];
     }
     const uint64_t nl2 = ptx::f2(nl, nl), dl2 = ptx::f2(dl, dl);
-    if constexpr (C::kQdOInTmem) {
+    if (C::kQdOInTmem && cw == 0) {
       // row r of the Q and dO tiles (SW128 boxes of 64 columns: 16-byte chunk c of row r sits at
       // chunk c ^ (r & 7)) -> packed bf16 pairs -> TMEM columns kColQ / kColdO (packed like P)
       ptx::mbar_wait(qd_full, 0);
@@ -556,10 +573,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ptx::mbar_wait(&s_full[h], j & 1);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-          bwd_ew_chunk<false>(tS + h * 64 + c * 32, tP + h * 64 + c * 32, tS + h * 64 + c * 16,
-                              tP + h * 64 + c * 16, h * 64 + c * 32, valid_k, sc2, &nl2, &dl2,
+        for (int cc = 0; cc < (kEW8 ? 1 : 2); ++cc) {
+          const int c = kEW8 ? cw : cc;
+          bwd_ew_chunk<false>(tS + h * 64 + c * 32, tP + h * 64 + c * 32, tS + h * 64 + ew_ocol(c),
+                              tP + h * 64 + ew_ocol(c), h * 64 + c * 32, valid_k, sc2, &nl2, &dl2,
                               false);
+        }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
@@ -570,7 +589,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     ptx::tc_fence_after();
     const bool live = r < min(128, tp.seg_len[a] - q_off);
     const int64_t idx = int64_t(tp.seg_dst[a] + q_off + r) * tp.BH + bh;
-    bwd_store_acc<D>(tmem + lane_base + C::kColA0, dq_acc + idx * D, scale, live);
+    if (kEW8)   // each warp of the pair adds half of the D columns
+      bwd_store_acc<D / 2>(tmem + lane_base + C::kColA0 + cw * (D / 2),
+                           dq_acc + idx * D + cw * (D / 2), scale, live);
+    else
+      bwd_store_acc<D>(tmem + lane_base + C::kColA0, dq_acc + idx * D, scale, live);
   }
 
   ptx::tc_fence_before();
