@@ -185,6 +185,67 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
   std::vector<Seg> node;
   int64_t gi = 0;
   const int64_t nmy = int64_t(p->my_order.size());
+
+  // Device-tier accumulator (j = 0): a row is final after the last task that merges into it (its
+  // segment is an active query segment of that task), so its O / lse are converted and downloaded
+  // right after that task instead of after the whole tree — the output D2H overlaps the remaining
+  // tasks (at depth 1, 4 of the 7 chunks are final before the last task).  fin[ti] = the row
+  // ranges whose last task is ti, from a sweep over the active query segments of every task.
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> fin;
+  if (j == 0 && nmy > 0) {
+    std::vector<std::pair<int64_t, int64_t>> ev;   // (row, +(ti+1) at start / -(ti+1) at end)
+    for (int64_t ti = 0; ti < nmy; ++ti) {
+      const Task& T = p->tasks[size_t(p->my_order[size_t(ti)])];
+      const Seg* sg = &p->segs[size_t(T.seg_off)];
+      for (int a = 0; a < T.nseg; ++a)
+        if (T.kept[a] && sg[a].len > 0) {
+          ev.push_back({sg[a].start, ti + 1});
+          ev.push_back({sg[a].start + sg[a].len, -(ti + 1)});
+        }
+    }
+    std::sort(ev.begin(), ev.end());
+    std::vector<int64_t> open_cnt(size_t(nmy) + 1, 0);   // covering tasks, by index
+    std::vector<int64_t> heap;                            // max-heap of open task indices
+    fin.assign(size_t(nmy), {});
+    int64_t row = 0;
+    size_t e = 0;
+    while (row < N) {
+      while (e < ev.size() && ev[e].first <= row) {       // apply every event at `row`
+        const int64_t t = ev[e].second;
+        if (t > 0) {
+          if (open_cnt[size_t(t)]++ == 0) {
+            heap.push_back(t);
+            std::push_heap(heap.begin(), heap.end());
+          }
+        } else {
+          --open_cnt[size_t(-t)];
+        }
+        ++e;
+      }
+      while (!heap.empty() && open_cnt[size_t(heap.front())] == 0) {
+        std::pop_heap(heap.begin(), heap.end());
+        heap.pop_back();
+      }
+      const int64_t next = e < ev.size() ? std::min<int64_t>(ev[e].first, N) : N;
+      // rows no task of this rank touches (none at world 1) are emitted after the last task
+      const int64_t last = heap.empty() ? nmy : heap.front();
+      auto& v = fin[size_t(last - 1)];
+      if (!v.empty() && v.back().first + v.back().second == row)
+        v.back().second += next - row;
+      else
+        v.push_back({row, next - row});
+      row = next;
+    }
+  }
+  auto emit_rows = [&](int64_t r0, int64_t len) -> cqs_status {   // j = 0: acc row = global row
+    for (int64_t c0 = 0; c0 < len; c0 += F) {
+      const int64_t n = std::min(F, len - c0);
+      cqs_status s2 = emit_final(fb_acquire(), acc_o + (r0 + c0) * BH * D,
+                                 acc_l + (r0 + c0) * BH, r0 + c0, n);
+      if (s2 != CQS_OK) return s2;
+    }
+    return CQS_OK;
+  };
   while (gi < nmy) {
     // ---- one depth-j subtree: tasks sharing quorum prefix (q_1..q_j) ----
     const Task& T0 = p->tasks[size_t(p->my_order[size_t(gi)])];
@@ -242,20 +303,20 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       CK(cudaEventRecord(ev_free[b], st));
       buf_used[b] = true;
       ++run;
+      if (j == 0)
+        for (const auto& iv : fin[size_t(ti)]) {
+          cqs_status s2 = emit_rows(iv.first, iv.second);
+          if (s2 != CQS_OK) return s2;
+        }
     }
 
     // ---- flush the subtree accumulator (pipelined over the two flush buffers) ----
     if (j > 0 && flushed_once) CK(cudaStreamWaitEvent(sc.fh, flush_done, 0));  // host rows settled
-    for (size_t s = 0; s < node.size(); ++s) {
+    for (size_t s = 0; s < node.size() && j > 0; ++s) {   // (j = 0: emitted task by task above)
       for (int64_t c0 = 0; c0 < node[s].len; c0 += F) {
         const int64_t n = std::min(F, node[s].len - c0);
         const int64_t grow = node[s].start + c0, lrow = node_off[s] + c0;
         const int b = fb_acquire();
-        if (j == 0) {
-          cqs_status s2 = emit_final(b, acc_o + lrow * BH * D, acc_l + lrow * BH, grow, n);
-          if (s2 != CQS_OK) return s2;
-          continue;
-        }
         CK(cudaMemcpyAsync(fb_o[b], hacc_o + grow * BH * D, size_t(n * BH * D * 4),
                            cudaMemcpyHostToDevice, sc.fh));
         CK(cudaMemcpyAsync(fb_l[b], hacc_l + grow * BH, size_t(n * BH * 4),

@@ -11,6 +11,11 @@
 using namespace cqs;
 
 __device__ unsigned long long g_cyc[64];
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 
 template <int VARIANT>
 __global__ void __launch_bounds__(256, 1) k(int iters, float* out) {
@@ -33,6 +38,7 @@ __global__ void __launch_bounds__(256, 1) k(int iters, float* out) {
   float m = 1.0f, l = 0.f, rmax_acc = 0.f;
   __syncwarp();
   const long long t0 = clock64();
+#pragma unroll 1
   for (int it = 0; it < iters; ++it) {
     uint32_t sr[128];
 #pragma unroll
@@ -48,7 +54,9 @@ __global__ void __launch_bounds__(256, 1) k(int iters, float* out) {
 #pragma unroll
       for (int ii = 0; ii < 16; ++ii) {
         const int i = 16 * c + ii;
-        if (VARIANT != 2 && (ii & 1) == 0)
+        if (VARIANT == 3)
+          mx4[ii & 3] = max3(mx4[ii & 3], s[2 * i], s[2 * i + 1]);
+        else if (VARIANT != 2 && (ii & 1) == 0)
           mx4[(i >> 1) & 3] = fmaxf(mx4[(i >> 1) & 3], fmaxf(fmaxf(s[2 * i], s[2 * i + 1]),
                                                              fmaxf(s[2 * i + 2], s[2 * i + 3])));
         float x0, x1;
@@ -106,7 +114,7 @@ int main() {
   for (int w : {4, 8}) {
     run<0>("exp pass + max + tcgen05.ld/st", w, d);
     run<1>("exp pass + max, no tcgen05.st", w, d);
-    run<2>("exp pass, no max", w, d);
+    run<3>("exp pass + max3 per pair", w, d);
   }
   return 0;
 }
