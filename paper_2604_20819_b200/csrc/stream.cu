@@ -278,6 +278,26 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       }
       const int b = int(run % S);
       if (buf_used[b]) CK(cudaStreamWaitEvent(sc.cs, ev_free[b], 0));
+      auto launch = [&](const Task& Tl) -> cqs_status {
+        TaskParams tp;
+        build_task_params_ext(p, Tl, d.in_dtype == CQS_BF16 ? attn_rows_per_item(d.D) : 32, src,
+                              dst, tp);
+        if (d.in_dtype == CQS_BF16)
+          CK(launch_attn_bf16(d.D, maps[b], tp, acc_o, acc_l, scale, st));
+        else
+          CK(launch_attn_f32(d.D, tp, reinterpret_cast<const float*>(stage[b][0]),
+                             reinterpret_cast<const float*>(stage[b][1]),
+                             reinterpret_cast<const float*>(stage[b][2]), sstr, acc_o, acc_l,
+                             scale, st));
+        ++launches;
+        return CQS_OK;
+      };
+      // The first task has nothing to overlap its staging with, so it runs segment by segment as
+      // its data lands: after segment x arrives, one launch covers the kept (query, key) segment
+      // pairs whose later segment is x.  Splitting a task's key set over launches is exact: each
+      // launch LSE-merges its partial into the accumulator like a task (Eq. 3).
+      const bool split_first = run == 0 && __builtin_popcount(used) > 1;
+      uint32_t arrived = 0;
       for (int a = 0; a < T.nseg; ++a) {
         if (!(used >> a & 1)) continue;
         for (int t = 0; t < 3; ++t)
@@ -286,20 +306,29 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
                                size_t(segs[a].len * D * e_in), size_t(BH),
                                cudaMemcpyHostToDevice, sc.cs));
         h2d += uint64_t(3 * segs[a].len * D * e_in * BH);
+        if (split_first) {
+          arrived |= 1u << a;
+          Task Tp = T;
+          bool any = false;
+          for (int x = 0; x < T.nseg; ++x) {
+            Tp.kept[x] = x == a ? T.kept[x] & arrived
+                                : ((arrived >> x & 1) ? T.kept[x] & (1u << a) : 0u);
+            any |= Tp.kept[x] != 0;
+          }
+          if (!any) continue;
+          cudaEvent_t seg_ready = sc.ev();
+          CK(cudaEventRecord(seg_ready, sc.cs));
+          CK(cudaStreamWaitEvent(st, seg_ready, 0));
+          cqs_status s2 = launch(Tp);
+          if (s2 != CQS_OK) return s2;
+        }
       }
-      CK(cudaEventRecord(ev_ready[b], sc.cs));
-      CK(cudaStreamWaitEvent(st, ev_ready[b], 0));
-      TaskParams tp;
-      build_task_params_ext(p, T, d.in_dtype == CQS_BF16 ? attn_rows_per_item(d.D) : 32, src, dst,
-                            tp);
-      if (d.in_dtype == CQS_BF16)
-        CK(launch_attn_bf16(d.D, maps[b], tp, acc_o, acc_l, scale, st));
-      else
-        CK(launch_attn_f32(d.D, tp, reinterpret_cast<const float*>(stage[b][0]),
-                           reinterpret_cast<const float*>(stage[b][1]),
-                           reinterpret_cast<const float*>(stage[b][2]), sstr, acc_o, acc_l,
-                           scale, st));
-      ++launches;
+      if (!split_first) {
+        CK(cudaEventRecord(ev_ready[b], sc.cs));
+        CK(cudaStreamWaitEvent(st, ev_ready[b], 0));
+        cqs_status s2 = launch(T);
+        if (s2 != CQS_OK) return s2;
+      }
       CK(cudaEventRecord(ev_free[b], st));
       buf_used[b] = true;
       ++run;
