@@ -323,20 +323,51 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
           if (s2 != CQS_OK) return s2;
         }
       }
+      // The last task has nothing after it to overlap the output download with, so it runs query
+      // segment by query segment and each segment's final rows are downloaded while the next
+      // segment computes (device-tier accumulator only).
+      const bool split_last = j == 0 && !split_first && ti == nmy - 1 &&
+                              [&] { int n = 0; for (int a = 0; a < T.nseg; ++a) n += T.kept[a] != 0; return n; }() > 1;
       if (!split_first) {
         CK(cudaEventRecord(ev_ready[b], sc.cs));
         CK(cudaStreamWaitEvent(st, ev_ready[b], 0));
-        cqs_status s2 = launch(T);
-        if (s2 != CQS_OK) return s2;
+        if (!split_last) {
+          cqs_status s2 = launch(T);
+          if (s2 != CQS_OK) return s2;
+        }
       }
+      std::vector<std::pair<int64_t, int64_t>> rest;   // final rows of this task still to emit
+      if (j == 0) rest = fin[size_t(ti)];
+      if (split_last)
+        for (int a = 0; a < T.nseg; ++a) {
+          if (!T.kept[a]) continue;
+          Task Tp = T;
+          for (int x = 0; x < T.nseg; ++x) Tp.kept[x] = x == a ? T.kept[x] : 0u;
+          cqs_status s2 = launch(Tp);
+          if (s2 != CQS_OK) return s2;
+          // rows of segment a whose last task is this one: emit them now, keep the remainder
+          const int64_t lo = segs[a].start, hi = segs[a].start + segs[a].len;
+          std::vector<std::pair<int64_t, int64_t>> keep;
+          for (const auto& iv : rest) {
+            const int64_t s0 = std::max(iv.first, lo), s1 = std::min(iv.first + iv.second, hi);
+            if (s0 >= s1) {
+              keep.push_back(iv);
+              continue;
+            }
+            s2 = emit_rows(s0, s1 - s0);
+            if (s2 != CQS_OK) return s2;
+            if (iv.first < s0) keep.push_back({iv.first, s0 - iv.first});
+            if (s1 < iv.first + iv.second) keep.push_back({s1, iv.first + iv.second - s1});
+          }
+          rest.swap(keep);
+        }
       CK(cudaEventRecord(ev_free[b], st));
       buf_used[b] = true;
       ++run;
-      if (j == 0)
-        for (const auto& iv : fin[size_t(ti)]) {
-          cqs_status s2 = emit_rows(iv.first, iv.second);
-          if (s2 != CQS_OK) return s2;
-        }
+      for (const auto& iv : rest) {
+        cqs_status s2 = emit_rows(iv.first, iv.second);
+        if (s2 != CQS_OK) return s2;
+      }
     }
 
     // ---- flush the subtree accumulator (pipelined over the two flush buffers) ----
