@@ -388,6 +388,42 @@ def main():
                "acc_depth": ps.info().acc_depth, "stage_buffers": ps.info().n_stage_buffers}
         del hq, hk, hv, ho, hl, sws, shws
 
+    # ---- end-to-end at N > 1 (streamed mode is single-GPU): every step H2D-copies the full Q/K/V
+    #      from pinned host memory to each rank (tasks read arbitrary rows), runs the plan +
+    #      task-sharded forward + exchange, and D2H-copies the rank's owned rows of O / lse ----
+    if not args.no_e2e and world > 1:
+        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+        ho = torch.empty((B, H, my_rows, D), dtype=out.dtype).pin_memory()
+        hl = torch.empty((B, H, my_rows), dtype=lse.dtype).pin_memory()
+
+        def e2e_step():
+            for dt_, ht in ((q, hq), (k, hk), (v, hv)):
+                dt_.copy_(ht, non_blocking=True)
+            step(False)
+            ho.copy_(out[:, :, row0:row0 + my_rows], non_blocking=True)
+            hl.copy_(lse[:, :, row0:row0 + my_rows], non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = max(1, min(args.steps, 3))
+        f0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([f0.elapsed_time(f1) / n_e2e],
+                         device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+        e2e = {"value": flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 3 * q.numel() * q.element_size(),
+               "d2h_bytes_per_step": ho.numel() * ho.element_size() + hl.numel() * 4,
+               "path": "per rank: full Q/K/V H2D from pinned host, cqs_attention_forward (resident, "
+                       "task-sharded) + exchange, owned O / lse rows D2H"}
+        del hq, hk, hv, ho, hl
+
     if rank != 0:
         dist.destroy_process_group()
         return 0
