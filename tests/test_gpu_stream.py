@@ -172,3 +172,21 @@ def test_streamed_mixed_level_interest_sets():
     Od, ld = O.dense_attention(*(t.double().numpy() for t in (q, k, v)))
     assert np.abs(out.double().numpy() - Od).max() <= 2e-2
     assert np.abs(lse.double().numpy() - ld).max() <= 1e-3
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("N,depth,nb", [(1, 0, 2), (300, 0, 2), (777, 1, 2), (2401, 2, 2),
+                                        (1500, 3, 2)])
+def test_streamed_device_tier_first_last_split(N, depth, nb, D):
+    """Device-tier accumulator (j = 0): the first task runs segment by segment as its staging
+    lands, the last task query segment by query segment, and every row is downloaded right after
+    its last task — each launch LSE-merges a partial over a key subset, so the result must still
+    equal dense attention; ragged sizes, depth 0 (a single task) to 3."""
+    H = 2
+    q, k, v = host_qkv(1, H, N, D, 91 + N + D, torch.bfloat16)
+    d = cqs.make_desc(N=N, B=1, H=H, D=D, depth=-1, in_dtype="bf16", qkv_loc="host")
+    budget = cqs.cqs_memory_model(d, depth, 0, nb)[0]
+    out, lse, info, st, peak = run_streamed(q, k, v, budget, depth=depth)
+    assert (info.depth, info.acc_depth, info.n_stage_buffers) == (depth, 0, nb)
+    assert peak <= budget + 512
+    check(out, lse, q, k, v, 2e-2, 1e-3)
