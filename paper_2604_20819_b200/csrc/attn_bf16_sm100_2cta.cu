@@ -31,7 +31,10 @@ constexpr int kThreads = 384;
 constexpr int kQBytes = kBM * D * 2;           // one 128-row Q tile (two 64-col boxes)
 constexpr int kKHalfRows = kBN / 2;            // keys per CTA in a K tile
 constexpr int kStageBytes = 16384;             // K half (2 boxes of 64 rows) or V half (1 box)
-constexpr int kStages = 8;
+#ifndef CQS_PAIR_STAGES
+#define CQS_PAIR_STAGES 8
+#endif
+constexpr int kStages = CQS_PAIR_STAGES;
 constexpr int kSmemBytes = 2 * kQBytes + kStages * kStageBytes + 1024 + 512;
 constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 384;
 constexpr float kRescaleThreshold = 8.0f;
