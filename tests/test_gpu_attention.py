@@ -112,10 +112,12 @@ def test_deterministic():
     assert torch.equal(a, b) and torch.equal(la, lb)
 
 
-def test_c2_full_size_sampled_rows():
+@pytest.mark.parametrize("D", [128, 64])
+def test_c2_full_size_sampled_rows(D):
     """BASELINE config 1 at full size (N=131072, H=32, D=128, bf16, one level), launched exactly as
-    bench.py does; 128 sampled (head, row) outputs against the oracle's blockwise dense rows."""
-    B, H, N, D = 1, 32, 131072, 128
+    bench.py does (and the same shape at C5's head dim D=64); 128 sampled (head, row) outputs
+    against the oracle's blockwise dense rows."""
+    B, H, N = 1, 32, 131072
     q, k, v = gen(B, H, N, D, 20260418, bf16=True)
     out, lse = cqs.attention(q, k, v, depth=1)
     torch.cuda.synchronize()
