@@ -139,12 +139,14 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
   };
   // final O/lse for rows [r0, r0+n) from an fp32 [n][BH][D] + [n][BH] source on the device,
   // staged as [BH][F][D] out + [BH][F] lse in flush buffer `b` and downloaded on sc.fd
-  auto emit_final = [&](int b, const float* src_o, const float* src_l, int64_t r0,
-                        int64_t n) -> cqs_status {
+  // (with part_o / part_l: the final rows are the LSE merge of that partial and src)
+  auto emit_final = [&](int b, const float* src_o, const float* src_l, int64_t r0, int64_t n,
+                        const float* part_o = nullptr, const float* part_l = nullptr) -> cqs_status {
     const int64_t ostr[4] = {int64_t(d.H) * F * D, F * D, D, 1};
     void* ob = fb_o[b];
     float* lb = fb_l[b];
-    CK(launch_merge(n, d.B, d.H, d.D, 0, nullptr, nullptr, const_cast<float*>(src_o),
+    CK(launch_merge(n, d.B, d.H, d.D, part_o ? 1 : 0, part_o ? &part_o : nullptr,
+                    part_l ? &part_l : nullptr, const_cast<float*>(src_o),
                     const_cast<float*>(src_l), false, ob, d.out_dtype, ostr, 0, F, lb, st));
     ++launches;
     CK(cudaEventRecord(fb_merged[b], st));
@@ -237,6 +239,67 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       row = next;
     }
   }
+  // Host-tier accumulators (j > 0): a row is final after the flush of the last depth-j subtree
+  // that contains it; at that flush its merged value is converted and downloaded straight from the
+  // flush buffers instead of being written back to the host accumulator and re-read by a final
+  // pass.  fin_g[g] = the row ranges whose last subtree is g (same sweep as fin, over the nodes).
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> fin_g;
+  bool direct_final = false;
+  if (j > 0 && nmy > 0) {
+    std::vector<std::pair<int64_t, int64_t>> ev;
+    int64_t ng = 0;
+    std::vector<Seg> nd;
+    for (int64_t g0 = 0; g0 < nmy; ++ng) {
+      const Task& A = p->tasks[size_t(p->my_order[size_t(g0)])];
+      int64_t g1 = g0 + 1;
+      while (g1 < nmy &&
+             std::equal(A.quorum, A.quorum + j, p->tasks[size_t(p->my_order[size_t(g1)])].quorum))
+        ++g1;
+      build_segments(N, p->lv, A.quorum, j, nd);
+      for (const Seg& sg : nd)
+        if (sg.len > 0) {
+          ev.push_back({sg.start, ng + 1});
+          ev.push_back({sg.start + sg.len, -(ng + 1)});
+        }
+      g0 = g1;
+    }
+    std::sort(ev.begin(), ev.end());
+    std::vector<int64_t> open_cnt(size_t(ng) + 1, 0), heap;
+    fin_g.assign(size_t(ng), {});
+    direct_final = true;
+    int64_t row = 0;
+    size_t e = 0;
+    while (row < N) {
+      while (e < ev.size() && ev[e].first <= row) {
+        const int64_t t = ev[e].second;
+        if (t > 0) {
+          if (open_cnt[size_t(t)]++ == 0) {
+            heap.push_back(t);
+            std::push_heap(heap.begin(), heap.end());
+          }
+        } else {
+          --open_cnt[size_t(-t)];
+        }
+        ++e;
+      }
+      while (!heap.empty() && open_cnt[size_t(heap.front())] == 0) {
+        std::pop_heap(heap.begin(), heap.end());
+        heap.pop_back();
+      }
+      const int64_t next = e < ev.size() ? std::min<int64_t>(ev[e].first, N) : N;
+      if (heap.empty()) {
+        direct_final = false;   // a row in no subtree (cannot happen at world 1): final pass
+      } else {
+        auto& v = fin_g[size_t(heap.front() - 1)];
+        if (!v.empty() && v.back().first + v.back().second == row)
+          v.back().second += next - row;
+        else
+          v.push_back({row, next - row});
+      }
+      row = next;
+    }
+  }
+  int64_t gidx = 0;   // subtree counter of the main loop (j > 0)
   auto emit_rows = [&](int64_t r0, int64_t len) -> cqs_status {   // j = 0: acc row = global row
     for (int64_t c0 = 0; c0 < len; c0 += F) {
       const int64_t n = std::min(F, len - c0);
@@ -372,10 +435,28 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
 
     // ---- flush the subtree accumulator (pipelined over the two flush buffers) ----
     if (j > 0 && flushed_once) CK(cudaStreamWaitEvent(sc.fh, flush_done, 0));  // host rows settled
+    const std::vector<std::pair<int64_t, int64_t>>* fg =
+        direct_final ? &fin_g[size_t(gidx)] : nullptr;
     for (size_t s = 0; s < node.size() && j > 0; ++s) {   // (j = 0: emitted task by task above)
-      for (int64_t c0 = 0; c0 < node[s].len; c0 += F) {
-        const int64_t n = std::min(F, node[s].len - c0);
+      for (int64_t c0 = 0; c0 < node[s].len;) {
         const int64_t grow = node[s].start + c0, lrow = node_off[s] + c0;
+        int64_t n = std::min(F, node[s].len - c0);
+        bool final_rows = false;
+        if (fg) {   // cut the run at the next final / non-final boundary
+          // node segments come in the node's chunk order (I order), not in row order: look up
+          // the first fin_g interval that ends after `grow`
+          size_t fk = size_t(std::upper_bound(fg->begin(), fg->end(), grow,
+                                              [](int64_t r, const std::pair<int64_t, int64_t>& iv) {
+                                                return r < iv.first + iv.second;
+                                              }) - fg->begin());
+          if (fk < fg->size() && (*fg)[fk].first <= grow) {
+            final_rows = true;
+            n = std::min(n, (*fg)[fk].first + (*fg)[fk].second - grow);
+          } else if (fk < fg->size()) {
+            n = std::min(n, (*fg)[fk].first - grow);
+          }
+        }
+        c0 += n;
         const int b = fb_acquire();
         CK(cudaMemcpyAsync(fb_o[b], hacc_o + grow * BH * D, size_t(n * BH * D * 4),
                            cudaMemcpyHostToDevice, sc.fh));
@@ -385,6 +466,13 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
         CK(cudaStreamWaitEvent(st, fb_loaded[b], 0));
         const float* po = acc_o + lrow * BH * D;
         const float* pl = acc_l + lrow * BH;
+        h2d += uint64_t(n * BH * (D + 1) * 4);
+        if (final_rows) {   // merge + convert into the other flush buffer, download O / lse
+          cqs_status s2 = emit_final(fb_acquire(), fb_o[b], fb_l[b], grow, n, po, pl);
+          if (s2 != CQS_OK) return s2;
+          CK(cudaEventRecord(fb_free[b], st));   // input consumed by the merge kernel
+          continue;
+        }
         CK(launch_merge(n, d.B, d.H, d.D, 1, &po, &pl, fb_o[b], fb_l[b], true, nullptr,
                         d.out_dtype, nullptr, 0, n, nullptr, st));
         ++launches;
@@ -395,10 +483,10 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
         CK(cudaMemcpyAsync(hacc_l + grow * BH, fb_l[b], size_t(n * BH * 4), cudaMemcpyDeviceToHost,
                            sc.fd));
         CK(cudaEventRecord(fb_free[b], sc.fd));
-        h2d += uint64_t(n * BH * (D + 1) * 4);
         d2h += uint64_t(n * BH * (D + 1) * 4);
       }
     }
+    ++gidx;
     if (j > 0) {
       CK(cudaEventRecord(flush_done, sc.fd));
       flushed_once = true;
@@ -406,7 +494,7 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
     gi = ge;
   }
 
-  if (j > 0) {  // host accumulator -> O, lse (after every flush has landed): in = fb 0, out = fb 1
+  if (j > 0 && !direct_final) {  // host accumulator -> O, lse (after every flush): in = fb 0, out = fb 1
     CK(cudaEventRecord(flush_done, sc.fd));
     CK(cudaStreamWaitEvent(sc.fh, flush_done, 0));
     for (int64_t r = 0; r < N; r += F) {
