@@ -469,6 +469,11 @@ def main():
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
         "backward": bwd,
     }
+    if bwd is not None:   # backward kernels against the same tensor peak (executed FLOPs: 14·N²·D)
+        bwd["roofline"] = {"bound": "tensor", "achieved": bwd["kernel_tflops_executed"],
+                           "peak": peak, "unit": "TFLOP/s",
+                           "frac": bwd["kernel_tflops_executed"] / peak,
+                           "kernels": "bwd_dkdv + bwd_dq", "peak_source": line["roofline"]["peak_source"]}
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
