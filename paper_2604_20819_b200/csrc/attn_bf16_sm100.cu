@@ -73,7 +73,10 @@ struct AttnCfg {
   static constexpr int kBoxes = D / 64;                // 64-column (128-byte) TMA boxes
   static constexpr int kQBytes = kBM * D * 2;
   static constexpr int kKVBytes = kBN * D * 2;
-  static constexpr int kStages = D == 128 ? 4 : 8;
+#ifndef CQS_ONE_STAGES64
+#define CQS_ONE_STAGES64 8
+#endif
+  static constexpr int kStages = D == 128 ? 4 : CQS_ONE_STAGES64;
   static constexpr int kSmemBytes = 2 * kQBytes + kStages * kKVBytes + 1024 + 512;
   static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
   // D = 64: Q lives in TMEM (A operand of S = Q K^T from TMEM, kind::f16 packed like P), so the
