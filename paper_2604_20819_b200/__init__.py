@@ -243,7 +243,20 @@ def _stream_ptr(stream):
 
 def cqs_attention_forward(plan: Plan, q, k, v, out, lse=None, scale=0.0, budget_bytes=0,
                           dev_ws=None, host_ws=None, stream=None, stats=False):
-    """q/k/v/out: torch tensors [B,H,N,D] (stride(D)=1); lse: fp32 [B,H,N] contiguous or None."""
+    """q/k/v/out: torch tensors [B,H,N,D] (stride(D)=1); lse: fp32 [B,H,N] contiguous or None.
+    k and v must share q's dtype and strides (the C ABI takes one stride array for all three)."""
+    import torch
+    for t in (k, v):
+        if tuple(t.stride()) != tuple(q.stride()) or t.dtype != q.dtype or t.shape != q.shape:
+            raise ValueError("q, k, v must share one shape, dtype and layout")
+    want = CQS_BF16 if q.dtype == torch.bfloat16 else (CQS_F32 if q.dtype == torch.float32 else -1)
+    if want != plan.desc.in_dtype:
+        raise ValueError("q dtype %s does not match the plan's in_dtype" % q.dtype)
+    if plan.desc.qkv_loc == CQS_LOC_PINNED_HOST and not (q.is_contiguous() and k.is_contiguous()
+                                                         and v.is_contiguous()):
+        raise ValueError("streamed (pinned host) q, k, v must be contiguous [B,H,N,D]")
+    if lse is not None and (lse.dtype != torch.float32 or not lse.is_contiguous()):
+        raise ValueError("lse must be a contiguous float32 [B,H,N] tensor")
     st = Stats() if stats else None
     _check(lib().cqs_attention_forward(
         plan.handle, _ptr(q), _ptr(k), _ptr(v), _i64x4(q.stride()), _ptr(out),
@@ -263,9 +276,15 @@ def cqs_attention_backward(plan: Plan, q, k, v, o, dout, lse, dq, dk, dv, scale=
                            stream=None, stats=False):
     """q/k/v/o/dout: bf16 device tensors [B,H,N,D] sharing one layout (stride(D)=1); lse: fp32
     [B,H,N] contiguous (the forward's); dq/dk/dv: [B,H,N,D] of the plan's out dtype, one layout."""
+    import torch
+    for t in (q, k, v, o, dout):
+        if t.dtype != torch.bfloat16:
+            raise ValueError("q, k, v, o, dout must be bfloat16 (the backward kernels read bf16)")
     for t in (k, v, o, dout):
         if tuple(t.stride()) != tuple(q.stride()):
             raise ValueError("q, k, v, o, dout must share one layout")
+    if lse.dtype != torch.float32 or not lse.is_contiguous():
+        raise ValueError("lse must be a contiguous float32 [B,H,N] tensor")
     for t in (dk, dv):
         if dq is not None and tuple(t.stride()) != tuple(dq.stride()):
             raise ValueError("dq, dk, dv must share one layout")

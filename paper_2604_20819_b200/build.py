@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "libcqs.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
-         "--expt-relaxed-constexpr", "-DCQS_WATCHDOG", "-I" + os.path.join(HERE, "..", "include")]
+         "--expt-relaxed-constexpr", "-I" + os.path.join(HERE, "..", "include")]
 
 
 def _sources():
@@ -38,7 +38,8 @@ def _compile(src, objdir=None, extra=()):
 
 
 def build(verbose: bool = False, variant: str = "", defines=()) -> str:
-    """variant/defines: debug timing variants (libcqs_<variant>.so); the product is the default."""
+    """variant/defines: debug / experiment variants (libcqs_<variant>.so, e.g. variant="dbg",
+    defines=["CQS_WATCHDOG"] for the mbarrier-wait watchdog); the product is the default."""
     objdir = OBJ + ("_" + variant if variant else "")
     lib = LIB if not variant else os.path.join(HERE, "libcqs_%s.so" % variant)
     os.makedirs(objdir, exist_ok=True)

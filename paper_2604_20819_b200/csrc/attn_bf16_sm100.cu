@@ -60,13 +60,8 @@ template <int D> constexpr uint32_t kPolyMask = 0x0;
 
 // Warpgroup ping-pong of the two tiles' softmax phases (named barriers 1 / 2).  Off: measured
 // slower at both head dims (D = 64: 651 vs 735 TFLOP/s; cycle counters in profiles/r01_notes.md).
-#ifdef CQS_DBG_PINGPONG
-template <int D>
-constexpr bool kPingPong = true;
-#else
 template <int D>
 constexpr bool kPingPong = false;
-#endif
 
 template <int D>
 struct AttnCfg {
@@ -82,11 +77,7 @@ struct AttnCfg {
   // D = 64: Q lives in TMEM (A operand of S = Q K^T from TMEM, kind::f16 packed like P), so the
   // S MMA reads only K from shared memory (an SS MMA at M = N = 128 needs the full 128 B/clk of
   // SMEM bandwidth, leaving none for the TMA fills).  D = 128 has no free TMEM columns for it.
-#ifdef CQS_DBG_Q_SMEM
-  static constexpr bool kQInTmem = false;
-#else
   static constexpr bool kQInTmem = D == 64;
-#endif
   static constexpr uint32_t kColQ0 = 256 + 2 * D, kColQ1 = 256 + 2 * D + D / 2;
 };
 
@@ -172,9 +163,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                            q_row + t * kBM, hi, bi);
       int it = 0;
       auto load = [&](const CUtensorMap* map, int row) {
-#ifdef CQS_DBG_NO_TMA_REFILL
-        if (it >= C::kStages) return;
-#endif
         const int s = it % C::kStages;
         const uint32_t ph = (it / C::kStages) & 1;
         ptx::mbar_wait(&kv_empty[s], ph ^ 1);
@@ -247,17 +235,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         int sKn = -1;
         if (j + 1 < n_kv) {
           sKn = it % C::kStages;
-#ifdef CQS_DBG_NO_TMA_REFILL
-          if (it < C::kStages)
-#endif
           ptx::mbar_wait(&kv_full[sKn], (it / C::kStages) & 1);
           ++it;
         }
         const int sV = it % C::kStages;
         DBG1_T0(tk0);
-#ifdef CQS_DBG_NO_TMA_REFILL
-        if (it < C::kStages)
-#endif
         ptx::mbar_wait(&kv_full[sV], (it / C::kStages) & 1);
         DBG1_T0(tk1);
 #ifdef CQS_DBG_TIMING
@@ -266,13 +248,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         ++it;
         ptx::tc_fence_after();
         for (int t = 0; t < (two ? 2 : 1); ++t) {
-#ifndef CQS_DBG_NO_PWAIT
           DBG1_T0(tw0);
           ptx::mbar_wait(&p_full[t], j & 1);
           DBG1_T0(tw1);
 #ifdef CQS_DBG_TIMING
           mma_pwait += tw1 - tw0;
-#endif
 #endif
           ptx::tc_fence_after();
           issue_PV(t, sV, j > 0);
@@ -326,17 +306,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         ptx::mbar_wait(&s_full[t], j & 1);
         ptx::tc_fence_after();
         DBG1_T0(ts1);
-#ifdef CQS_DBG_NO_PWAIT   // timing experiment only: softmax warps do nothing
-        break;
-#endif
         if (kPingPong<D> && two && !(t == 0 && j == 0)) ptx::named_bar_sync(1 + t, 256);
-#ifdef CQS_DBG_SKIP_SOFTMAX   // timing experiment only: tensor/TMA pipeline without softmax work
-        if (j == 0) m = 0.f, l = 1.f;
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&p_full[t]);
-        continue;
-#endif
         uint32_t sr[kBN];
 #pragma unroll
         for (int c = 0; c < kBN / 32; ++c)
@@ -498,47 +468,25 @@ static cudaError_t launch_bf16_impl(const CUtensorMap* maps, const TaskParams& t
 
 cudaError_t launch_attn_bf16_pair(const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
                                   float* acc_lse, float scale, cudaStream_t stream);
-cudaError_t launch_attn_bf16_d64(const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
-                                 float* acc_lse, float scale, cudaStream_t stream);
-int d64_rows_per_item();
-int d64_kv_box_rows();
 
 // D = 128 runs on CTA pairs (cta_group::2, 512 query rows per item; K maps with 64-row boxes);
-// D = 64 on the two-tile kernel above; -DCQS_D64_DBS routes it to the double-buffered-S
-// kernel (attn_bf16_sm100_d64.cu: parity-green, measured 680 vs 695 TFLOP/s on C2-d64).
+// D = 64 on the two-tile kernel above (a double-buffered-S alternative measured 680 vs 695
+// TFLOP/s on C2-d64; kept out of the build in tools/experiments/attn_bf16_sm100_d64.cu).
 // Callers size work items with attn_rows_per_item and build the Q / K / V maps with
 // attn_box_rows(D, 0 / 1 / 2).
 int attn_rows_per_item(int D) {
-#ifndef CQS_ONE_CTA_D128
   if (D == 128) return 512;
-#endif
-#ifdef CQS_D64_DBS
-  if (D == 64) return d64_rows_per_item();
-#endif
   return 256;
 }
 int attn_box_rows(int D, int which) {
-#ifndef CQS_ONE_CTA_D128
   if (D == 128 && which == 1) return 64;
-#endif
-#ifdef CQS_D64_DBS
-  if (D == 64 && which != 0) return d64_kv_box_rows();
-#endif
   return 128;
 }
 
 cudaError_t launch_attn_bf16(int D, const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
                              float* acc_lse, float scale, cudaStream_t stream) {
-#ifndef CQS_ONE_CTA_D128
   if (D == 128) return launch_attn_bf16_pair(maps, tp, acc_o, acc_lse, scale, stream);
-#else
-  if (D == 128) return launch_bf16_impl<128>(maps, tp, acc_o, acc_lse, scale, stream);
-#endif
-#ifdef CQS_D64_DBS
-  if (D == 64) return launch_attn_bf16_d64(maps, tp, acc_o, acc_lse, scale, stream);
-#else
   if (D == 64) return launch_bf16_impl<64>(maps, tp, acc_o, acc_lse, scale, stream);
-#endif
   return cudaErrorInvalidValue;
 }
 

@@ -55,11 +55,7 @@ static_assert(128 * (168 - CQS_PAIR_REG_LO) == 256 * (CQS_PAIR_REG_HI - 168), "r
 // TFLOP/s on C2, softmax wait-for-S 1808 vs 1207 cycles per tile): an N = 64 SS MMA still reads the
 // whole 4 KB Q slice per instruction, so the S halves exceed the 128 B/clk SMEM operand bandwidth.
 // Experiment only (-DCQS_SPLIT_S).
-#if defined(CQS_SPLIT_S) && !defined(CQS_DBG_NO_PWAIT)
-constexpr bool kSplitS = true;
-#else
 constexpr bool kSplitS = false;
-#endif
 // column pairs (i mod 8) whose exp2 runs as an FMA-pipe polynomial instead of MUFU.EX2
 #ifdef CQS_DBG_POLY_MASK
 constexpr uint32_t kPolyMask = CQS_DBG_POLY_MASK;
@@ -154,9 +150,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
                                q_row + t * 2 * kBM, hi, bi);
       int it = 0;
       auto stage_wait = [&](int s) {
-#ifdef CQS_DBG_NO_TMA_REFILL
-        if (it >= kStages) return false;
-#endif
         ptx::mbar_wait(&kv_empty[s], ((it / kStages) & 1) ^ 1);
         if (leader) ptx::mbar_arrive_expect_tx(&kv_full[s], 2 * kStageBytes);
         return true;
@@ -254,16 +247,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         int sKn = -1;
         if (j + 1 < n_kv) {
           sKn = it % kStages;
-#ifdef CQS_DBG_NO_TMA_REFILL
-          if (it < kStages)
-#endif
           ptx::mbar_wait(&kv_full[sKn], (it / kStages) & 1);
           ++it;
         }
         const int sV = it % kStages;
-#ifdef CQS_DBG_NO_TMA_REFILL
-        if (it < kStages)
-#endif
         ptx::mbar_wait(&kv_full[sV], (it / kStages) & 1);
         ++it;
         ptx::tc_fence_after();
@@ -273,13 +260,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
             ptx::tc_fence_after();
             issue_S_half(t, sKn, 0);
           }
-#ifndef CQS_DBG_NO_PWAIT
           DBG_T0(tw0);
           ptx::mbar_wait(&p_full[t], j & 1);
 #ifdef CQS_DBG_TIMING
           DBG_T0(tw1);
           mma_pwait += tw1 - tw0;
-#endif
 #endif
           ptx::tc_fence_after();
           issue_PV(t, sV, j > 0);
@@ -323,17 +308,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         DBG_T0(ts1);
 #ifdef CQS_DBG_TIMING
         dc[0] += ts1 - ts0, dc[2] += 1;
-#endif
-#ifdef CQS_DBG_NO_PWAIT   // timing experiment only: softmax warps do nothing
-        break;
-#endif
-#ifdef CQS_DBG_SKIP_SOFTMAX   // timing experiment only: MMA/TMA pipeline without softmax math
-        if (j == 0) m = 0.f, l = 1.f;
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_leader(&p_full[t]);
-        if (kSplitS && lane == 0) ptx::mbar_arrive_leader(&s_loaded[t]);
-        continue;
 #endif
         uint32_t sr[kBN];
         // registers in key order: with split S, keys [32c, 32c + 32) sit at column

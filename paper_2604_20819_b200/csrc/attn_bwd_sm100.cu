@@ -35,11 +35,7 @@ namespace cqs {
 // (one warp alone reaches ~79% of its rate, two ~89%: tools/softmax_bench.cu).  Each chunk's P / dS
 // (bf16 pairs) is written at the start of its own 32 source columns, so the two warps never write
 // columns the other still has to read; the MMAs read the A operand at ew_acol(kk).
-#ifdef CQS_BWD_EW4
-constexpr bool kEW8 = false;
-#else
 constexpr bool kEW8 = true;
-#endif
 constexpr int kBwdThreads = kEW8 ? 384 : 256;
 __device__ __forceinline__ constexpr uint32_t ew_ocol(int c) { return kEW8 ? c * 32 : c * 16; }
 __device__ __forceinline__ constexpr uint32_t ew_acol(int kk) {
@@ -61,19 +57,11 @@ struct BwdCfg {
   // from shared memory (an SS MMA at M = 128, N = 64 needs 192 B/clk of SMEM, over the 128 B/clk
   // available; with A in TMEM it needs 64)
   static constexpr uint32_t kColQ = 256 + D, kColdO = 256 + D + D / 2;
-#ifdef CQS_BWD_DQ_SMEM_A
-  static constexpr bool kQdOInTmem = false;
-#else
   static constexpr bool kQdOInTmem = true;
-#endif
   // dK/dV kernel at D = 64: the CTA's K and V tiles (A of S^T = K Q^T, dP^T = V dO^T) in TMEM after
   // the dK accumulator; at D = 128 the four 128-column regions use all 512 columns
   static constexpr uint32_t kColKT = 256 + 2 * D, kColVT = 256 + 2 * D + D / 2;
-#ifdef CQS_BWD_DKDV_SMEM_A
-  static constexpr bool kKVInTmem = false;
-#else
   static constexpr bool kKVInTmem = D == 64;
-#endif
 };
 
 // descriptor offset of the 16-wide K step `ks` in a K-major SW128 tile of 128 rows
@@ -663,22 +651,14 @@ static cudaError_t launch_bwd_impl(const CUtensorMap* maps, const TaskParams& tp
   return cudaGetLastError();
 }
 
-cudaError_t launch_attn_bwd_fused(const CUtensorMap* maps, const TaskParams& tp, const float* ld,
-                                  int64_t ld_pitch, int64_t N, float* dq, float* dk, float* dv,
-                                  float scale, cudaStream_t st);
-
 // maps: Q, K, V, dO (bf16, 128-row boxes); ld: fp32 [BH][2][pitch] (-lse*log2e, Delta).
-// Default: the dK/dV + dQ kernel pair above.  -DCQS_BWD_FUSED builds route D = 128 through the
-// single fused kernel (attn_bwd_fused_sm100.cu; dQ by fp32 L2 reductions): parity-green but 23%
-// slower on B200 — its red.global traffic (64 KB per 128x128 block) saturates the per-SM L2
+// The dK/dV + dQ kernel pair above.  A single fused kernel (tools/experiments/
+// attn_bwd_fused_sm100.cu, not built; dQ by fp32 L2 reductions) was parity-green but 23% slower on B200 — its red.global traffic (64 KB per 128x128 block) saturates the per-SM L2
 // reduction path (profiles/r01_notes.md).
 cudaError_t launch_attn_bwd_bf16(int D, const CUtensorMap* maps, const TaskParams& tpq,
                                  const TaskParams& tpk, const float* ld, int64_t ld_pitch,
                                  int64_t N, float* dq, float* dk, float* dv, float scale,
                                  cudaStream_t st) {
-#ifdef CQS_BWD_FUSED
-  if (D == 128) return launch_attn_bwd_fused(maps, tpk, ld, ld_pitch, N, dq, dk, dv, scale, st);
-#endif
   if (D == 128) return launch_bwd_impl<128>(maps, tpq, tpk, ld, ld_pitch, N, dq, dk, dv, scale, st);
   if (D == 64) return launch_bwd_impl<64>(maps, tpq, tpk, ld, ld_pitch, N, dq, dk, dv, scale, st);
   return cudaErrorInvalidValue;

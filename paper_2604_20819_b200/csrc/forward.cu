@@ -149,9 +149,15 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
   const auto t0 = std::chrono::steady_clock::now();
   uint8_t* ws = static_cast<uint8_t*>(dev_ws);
 
-  if (d.qkv_loc == CQS_LOC_PINNED_HOST)
+  if (d.qkv_loc == CQS_LOC_PINNED_HOST) {
+    // the staging copies address rows as base + row * D with pitch N * D: contiguous only
+    const int64_t N = d.N, D = d.D;
+    if (!qkv_strides || qkv_strides[0] != int64_t(d.H) * N * D || qkv_strides[1] != N * D ||
+        qkv_strides[2] != D || qkv_strides[3] != 1)
+      return fail(CQS_E_INVALID, "streamed Q/K/V must be contiguous [B,H,N,D]");
     return forward_streamed(p, q, k, v, out, out_strides, lse, scale, ws,
                             static_cast<uint8_t*>(host_ws), st, stats);
+  }
 
   if (!qkv_strides || qkv_strides[3] != 1)
     return fail(CQS_E_INVALID, "qkv strides: stride(D) must be 1");

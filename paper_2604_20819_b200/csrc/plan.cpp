@@ -438,13 +438,17 @@ cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
   int chosen = -1, chosen_j = 0, chosen_nbuf = 0;
   int64_t acc_rows = d.N;
   MemModel mm{};
+  if (!streamed) {
+    // resident bytes do not depend on the depth: decide feasibility once, then enumerate only
+    // the chosen depth (the smallest one, or the caller's)
+    mm = memory_model(d, 0, d.N, 0);
+    if (budget != 0 && mm.caller_dev + mm.dev_ws > budget)
+      return fail(CQS_E_INFEASIBLE, "resident plan exceeds budget_bytes at every depth");
+    if ((st = enumerate_leaves(d, lv, k_lo, ls)) != CQS_OK) return st;
+    chosen = k_lo;
+  }
   for (int k = k_lo; k <= k_hi && chosen < 0; ++k) {
     if ((st = enumerate_leaves(d, lv, k, ls)) != CQS_OK) return st;
-    if (!streamed) {
-      mm = memory_model(d, 0, d.N, 0);
-      if (budget == 0 || mm.caller_dev + mm.dev_ws <= budget) chosen = k;
-      continue;
-    }
     for (int nbuf = 2; nbuf >= 1 && chosen < 0; --nbuf)
       for (int j = 0; j <= k && chosen < 0; ++j) {
         const int64_t rows = max_node_rows(d.N, lv, j);
