@@ -32,7 +32,15 @@ CONFIGS = {
                   desc="small: N=16384, H=8, D=128, bf16, one CQS level"),
     "c2d64": dict(N=131072, B=1, H=32, D=64, depth=1, dtype="bf16",
                   desc="C2 with D=64 (C5 head dim), bf16, one CQS level, resident"),
+    # BASELINE.json configs[3]: the multi-GPU scaling workload (16M = 2^24, k = 3)
+    "c4": dict(N=1 << 24, B=1, H=8, D=128, depth=3, dtype="bf16", shard="contiguous",
+               desc="C4: N=2^24, H=8, D=128, bf16, three CQS levels (343 tasks), tasks sharded "
+                    "across ranks (contiguous DFS runs), one exchange"),
 }
+# C3 (BASELINE.json configs[2]): the "peak memory vs budget" half of the metric, run at N=1
+BUDGET_CFG = dict(N=1_000_000, B=1, H=32, D=128, budget=16 << 30, seed=20260419,
+                  desc="C3: N=1,000,000, H=32, D=128, bf16, Q/K/V/O in pinned host memory, "
+                       "16 GiB device budget -> depth from the memory model (streamed)")
 SEED = 20260418  # 20260417 + config index 1
 
 
@@ -174,6 +182,135 @@ def run_reference(args, cfg):
     return 0
 
 
+def lscpu_model():
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+class MemPoll:
+    """Device memory in use (NVML, whole device) sampled every ~2 ms in a thread: peak during a
+    region, as the driver accounts it (independent of torch's allocator)."""
+
+    def __init__(self, index):
+        self.index, self.peak, self.base = index, 0, 0
+
+    def __enter__(self):
+        import threading
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.get = lambda: pynvml.nvmlDeviceGetMemoryInfo(self.h).used
+            self.base = self.peak = self.get()
+        except Exception:
+            self.get = None
+            return self
+        self.stop = False
+
+        def run():
+            while not self.stop:
+                self.peak = max(self.peak, self.get())
+                time.sleep(0.002)
+
+        self.t = threading.Thread(target=run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.get is not None:
+            self.stop = True
+            self.t.join()
+            self.peak = max(self.peak, self.get())
+
+
+def shared_pinned(name, shape, dtype, fill, local_rank, local_world, barrier):
+    """A host tensor shared by the ranks of this node (/dev/shm file, so one copy serves every rank)
+    and page-locked in each process (cudaHostRegister).  `fill(t, i, n)` fills part i of n."""
+    import torch
+    n = 1
+    for x in shape:
+        n *= int(x)
+    esz = torch.tensor([], dtype=dtype).element_size()
+    path = "/dev/shm/cqs_bench_%s_%d" % (name, os.getppid())
+    if local_rank == 0:
+        with open(path, "wb") as f:
+            f.truncate(n * esz)
+    barrier()
+    t = torch.from_file(path, shared=True, size=n, dtype=dtype).view(*shape)
+    fill(t, local_rank, local_world)
+    barrier()
+    rc = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), n * esz, 0)
+    assert int(rc) == 0, "cudaHostRegister failed (%s)" % rc
+    barrier()
+    if local_rank == 0:
+        os.unlink(path)   # the mappings stay valid
+    return t
+
+
+def budget_run(dev, local):
+    """C3 under its 16 GiB budget: plan with depth -1 from the budget, Q/K/V/O
+    in pinned host memory, one warm-up and one timed step; device bytes predicted by the memory
+    model vs measured three ways: torch allocator peak, cudaMemGetInfo delta, NVML peak."""
+    import torch
+    import cqs_synth
+    import paper_2604_20819_b200 as cqs
+    c = BUDGET_CFG
+    N, B, H, D, budget = c["N"], c["B"], c["H"], c["D"], c["budget"]
+    hq, hk, hv = (cqs_synth.torch_tensor((B, H, N, D), c["seed"], nm, torch.bfloat16, dev)
+                  .cpu().pin_memory() for nm in ("q", "k", "v"))
+    ho = torch.empty((B, H, N, D), dtype=torch.bfloat16).pin_memory()
+    hl = torch.empty((B, H, N), dtype=torch.float32).pin_memory()
+    desc = dict(N=N, B=B, H=H, D=D, depth=-1, budget_bytes=budget, in_dtype="bf16",
+                qkv_loc="host", out_loc="host")
+    p = cqs.cqs_plan(**desc)
+    info = p.info()
+    dv, hb = cqs.cqs_forward_workspace_size(p)
+    hws = torch.empty(max(hb, 256), dtype=torch.uint8).pin_memory() if hb else None
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    torch.cuda.reset_peak_memory_stats(dev)
+    a0 = torch.cuda.memory_allocated(dev)
+    free0 = torch.cuda.mem_get_info(dev)[0]
+    stream = torch.cuda.current_stream()
+    with MemPoll(local) as mp:
+        ws = torch.empty(dv, dtype=torch.uint8, device=dev)
+        cqs.cqs_attention_forward(p, hq, hk, hv, ho, hl, 0.0, budget, ws, hws, stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            p2 = cqs.cqs_plan(**desc)
+            cqs.cqs_attention_forward(p2, hq, hk, hv, ho, hl, 0.0, budget, ws, hws, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        free1 = torch.cuda.mem_get_info(dev)[0]
+    ms = e0.elapsed_time(e1)
+    alloc_peak = torch.cuda.max_memory_allocated(dev) - a0
+    res = {"workload": c["desc"], "budget_bytes": budget, "depth": info.depth,
+           "acc_depth": info.acc_depth, "stage_buffers": info.n_stage_buffers,
+           "predicted_bytes": info.predicted_peak_bytes,
+           "measured_allocator_bytes": alloc_peak,
+           "measured_cudaMemGetInfo_bytes": free0 - free1,
+           "measured_nvml_peak_bytes": (mp.peak - mp.base) if mp.get else None,
+           "steps": 1, "warmup": 1, "ms_per_step": ms,
+           "value": 4.0 * N * N * D * B * H / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+           "clocks": clk.summary(),
+           "note": "device bytes of the call (caller tensors on the host): allocator = torch "
+                   "max_memory_allocated delta; cudaMemGetInfo = free-memory drop with the "
+                   "workspace live (2 MiB pages); nvml = device-wide peak during both steps"}
+    meas = [x for x in (alloc_peak, free0 - free1, res["measured_nvml_peak_bytes"]) if x is not None]
+    res["within_budget"] = bool(info.predicted_peak_bytes <= budget and max(meas) <= budget)
+    res["measured_vs_predicted"] = max(meas) / info.predicted_peak_bytes
+    del ws, hq, hk, hv, ho, hl, hws
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -181,14 +318,22 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cqs")
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--heads", type=int, default=0,
+                    help="override the config's head count (validation runs only: the line's "
+                         "config then says so)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-budget", action="store_true",
+                    help="skip the C3 16 GiB budget run (N=1 only)")
     ap.add_argument("--no-bwd", action="store_true",
                     help="skip the backward (Algorithm 2, SURVEY NEXT-1) measurement")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
-                    help="N>1: merge over peer memory in one kernel (p2p) or NCCL all-to-all + merge")
+                    help="N>1: merge over peer memory (p2p) or NCCL all-to-all + merge")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
+    if args.heads:
+        cfg["H"] = args.heads
+        cfg["desc"] += " [validation run: H overridden to %d]" % args.heads
     if args.impl == "reference":
         return run_reference(args, cfg)
 
@@ -201,6 +346,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    local_rank = local
     # CQS_SAME_DEVICE=1 + CQS_DIST_BACKEND=gloo: exercise the multi-rank code path with all ranks
     # on one GPU (validation only; NCCL refuses two ranks per device)
     if os.environ.get("CQS_SAME_DEVICE") == "1":
@@ -213,55 +360,99 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-        cfg["schedule"] = "hybrid"   # mixed-depth leaves: LPT makespan within 1% (NEXT-2, R20)
+        if "shard" not in cfg:
+            cfg["schedule"] = "hybrid"   # mixed-depth leaves: LPT makespan within 1% (NEXT-2, R20)
+    barrier = (lambda: dist.barrier()) if world > 1 else (lambda: None)
+    rdev = dev if (world > 1 and dist.get_backend() == "nccl") else "cpu"
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([float(x)], device=rdev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     N, B, H, D, depth = cfg["N"], cfg["B"], cfg["H"], cfg["D"], cfg["depth"]
     bf = cfg["dtype"] == "bf16"
     dt = torch.bfloat16 if bf else torch.float32
-    q, k, v = cqs_synth.torch_qkv(B, H, N, D, SEED, dtype=dt, device=dev)
-    out = torch.empty(B, H, N, D, dtype=dt, device=dev)
-    lse = torch.empty(B, H, N, dtype=torch.float32, device=dev)
-    desc_kw = dict(N=N, B=B, H=H, D=D, depth=depth, in_dtype=cfg["dtype"], world=world, rank=rank,
-                   schedule=cfg.get("schedule", "uniform"))
-    p0 = cqs.cqs_plan(**desc_kw)
-    info = p0.info()
-    dev_bytes, _ = cqs.cqs_forward_workspace_size(p0)
-    ws = torch.empty(dev_bytes, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream()
     BH = B * H
-
-    if world > 1:
-        row0, my_rows = cqs.cqs_shard_rows(N, world, rank)
-        ao, al = cqs.cqs_partial_view(p0, ws)
-        base = ws.data_ptr()
-        acc_o = ws[ao - base: ao - base + N * BH * D * 4].view(torch.float32).view(N, BH * D)
-        acc_l = ws[al - base: al - base + N * BH * 4].view(torch.float32).view(N, BH)
-        px = cdist.PeerExchange(p0, ws, N, B, H, D, world, rank) if args.exchange == "p2p" else None
-
     flops = 4.0 * N * N * D * BH
+    desc_kw = dict(N=N, B=B, H=H, D=D, depth=depth, in_dtype=cfg["dtype"], world=world, rank=rank,
+                   schedule=cfg.get("schedule", "uniform"), shard=cfg.get("shard", "lpt"))
+    # resident if this rank's plan fits the device (C4 at R <= 2 does not: streamed then)
+    p0 = cqs.cqs_plan(**desc_kw)
+    free_dev = torch.cuda.mem_get_info(dev)[0] // (local_world if os.environ.get("CQS_SAME_DEVICE") == "1" else 1)
+    resident = max_over_ranks(p0.info().predicted_peak_bytes) <= free_dev - (2 << 30)
+    if not resident:
+        desc_kw.update(qkv_loc="host", out_loc="host")
+        p0 = cqs.cqs_plan(**desc_kw)
+    info = p0.info()
+    row0, my_rows = cqs.cqs_shard_rows(N, world, rank) if world > 1 else (0, N)
+    stream = torch.cuda.current_stream()
+
+    def make_host_qkv():
+        if world == 1:
+            return tuple(cqs_synth.torch_tensor((B, H, N, D), SEED, nm, dt, dev).cpu().pin_memory()
+                         for nm in ("q", "k", "v"))
+
+        def filler(nm):
+            def fill(t, i, n):   # rank i of n fills heads i, i+n, ... (generated on the GPU)
+                for h in range(i, H, n):
+                    flat = t.view(-1)[h * N * D:(h + 1) * N * D]
+                    for s0 in range(0, N * D, 1 << 28):
+                        c = min(1 << 28, N * D - s0)
+                        flat[s0:s0 + c].copy_(cqs_synth.torch_values(
+                            SEED, cqs_synth.TID[nm], h * N * D + s0, c, dev).to(dt).cpu())
+            return fill
+        return tuple(shared_pinned(nm, (B, H, N, D), dt, filler(nm), local_rank, local_world,
+                                   barrier) for nm in ("q", "k", "v"))
+
+    host_qkv = None
+    if resident:
+        q, k, v = cqs_synth.torch_qkv(B, H, N, D, SEED, dtype=dt, device=dev)
+    else:
+        host_qkv = make_host_qkv()
+        q, k, v = host_qkv
+    out = torch.empty(B, H, my_rows, D, dtype=dt, device=dev)
+    lse = torch.empty(B, H, my_rows, dtype=torch.float32, device=dev)
+    hout = hlse = None
+    if not resident and world == 1:
+        hout = torch.empty(B, H, N, D, dtype=dt).pin_memory()
+        hlse = torch.empty(B, H, N, dtype=torch.float32).pin_memory()
+    dev_bytes, host_bytes = cqs.cqs_forward_workspace_size(p0)
+    ws = torch.empty(dev_bytes, dtype=torch.uint8, device=dev)
+    hws = torch.empty(max(host_bytes, 256), dtype=torch.uint8).pin_memory() if host_bytes else None
+    px = None
+    if world > 1 and args.exchange == "p2p":
+        px = cdist.PeerExchange(p0, ws)
 
     def step(with_stats):
         p = cqs.cqs_plan(**desc_kw)                      # a1: CQS Divide planning (host C++)
-        st = cqs.cqs_attention_forward(p, q, k, v, out, lse if world == 1 else None, 0.0, 0, ws,
-                                       None, stream, stats=with_stats)
-        if world > 1 and args.exchange == "p2p":      # a5: exchange + merge over NVLink, 1 kernel
+        if world == 1:
+            st = cqs.cqs_attention_forward(p, q, k, v, out if resident else hout,
+                                           lse if resident else hlse, 0.0, 0, ws, hws, stream,
+                                           stats=with_stats)
+        else:
+            st = cqs.cqs_attention_forward(p, q, k, v, None, None, 0.0, 0, ws, None, stream,
+                                           stats=with_stats)
+        if px is not None:                               # a5: exchange + merge over NVLink
             px.merge(out, lse, stream)
-        elif world > 1:                                   # a5: NCCL all-to-all + R-way merge
-            ro, rl, r0, nr = cdist.exchange_partials(acc_o, acc_l, N, world, rank)
-            cdist.merge_shard_gpu(ro, rl, world, nr, B, H, D, out, lse, r0, N, stream)
+        elif world > 1:                                  # a5: NCCL all-to-all + merge
+            acc_o, acc_l = cdist.partial_accumulator(p0, ws)
+            ro, rl, off, pr0 = cdist.exchange_partials(p0, acc_o, acc_l)
+            cdist.merge_received(p0, ro, rl, off, pr0, out, lse, stream)
         return st
 
     for _ in range(args.warmup):
         step(False)
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats(dev)   # peak over the timed region: caller tensors + ws
-    if world > 1:
-        dist.barrier()
+    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     attn_ms, merge_ms, launches = 0.0, 0.0, 0
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        barrier()
         e0.record(stream)
         for _ in range(args.steps):
             st = step(True)
@@ -270,34 +461,31 @@ def main():
             launches += st.kernel_launches
         e1.record(stream)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     timed_peak = torch.cuda.max_memory_allocated(dev)
     if world > 1:
-        rdev = dev if dist.get_backend() == "nccl" else "cpu"
-        t = torch.tensor([ms], device=rdev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        launches_t = torch.tensor([launches], device=rdev, dtype=torch.float64)
-        dist.all_reduce(launches_t)
-        launches = int(launches_t.item())
+        lt = torch.tensor([launches], device=rdev, dtype=torch.float64)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
+        if px is not None:   # one kernel per run of rows with the same holders, on every rank
+            launches += args.steps * world
+    kern_ms_max = max_over_ranks(attn_ms / args.steps)
 
-    # ---- backward (Algorithm 2, NEXT-1): dQ/dK/dV of sum(dO*O) for this step's O / lse, resident,
-    #      world = 1; its own line item, not part of the forward `value` ----
+    # ---- backward (Algorithm 2, NEXT-1): dQ/dK/dV of sum(dO*O), resident single-node tensors;
+    #      its own line item, not part of the forward `value` ----
     bwd = None
-    if not args.no_bwd and bf and D in (64, 128):
+    if not args.no_bwd and bf and D in (64, 128) and resident and args.config != "c4":
         do = cqs_synth.torch_tensor((B, H, N, D), SEED, "do", torch.bfloat16, dev)
-        if world > 1:   # O / lse of every row on every rank (untimed setup: the forward's output)
-            bo, bl = cqs.attention(q, k, v, depth=depth)
-        else:
-            bo, bl = out, lse
-        bws = torch.empty(cqs.cqs_backward_workspace_size(p0), dtype=torch.uint8, device=dev)
+        bo, bl = (out, lse) if world == 1 else cqs.attention(q, k, v, depth=depth)
+        bdesc = dict(desc_kw, shard="lpt")
+        pb = cqs.cqs_plan(**bdesc)
+        bws = torch.empty(cqs.cqs_backward_workspace_size(pb), dtype=torch.uint8, device=dev)
         dq, dk, dv = (torch.empty_like(q) for _ in range(3))
-        pgr = cdist.PeerGradReduce(p0, bws, N, B, H, D, world, rank) if world > 1 else None
+        pgr = cdist.PeerGradReduce(pb, bws, N, B, H, D, world, rank) if world > 1 else None
 
         def bstep(with_stats):
-            st = cqs.cqs_attention_backward(p0, q, k, v, bo, do, bl, dq, dk, dv, 0.0, bws,
+            st = cqs.cqs_attention_backward(pb, q, k, v, bo, do, bl, dq, dk, dv, 0.0, bws,
                                             stream, stats=with_stats)
             if pgr is not None:   # owner sums the ranks' partial rows over peer memory
                 pgr.reduce(dq, dk, dv, stream)
@@ -305,8 +493,7 @@ def main():
 
         bstep(False)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        barrier()
         n_b = max(1, min(args.steps, 3))
         b_attn = 0.0
         with ClockSampler(local) as bclk:
@@ -316,14 +503,11 @@ def main():
                 b_attn += bstep(True).ms_attn
             g1.record(stream)
             torch.cuda.synchronize()
-        b_ms = g0.elapsed_time(g1) / n_b
-        if world > 1:
-            t = torch.tensor([b_ms], device=dev if dist.get_backend() == "nccl" else "cpu")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            b_ms = float(t.item())
+        b_ms = max_over_ranks(g0.elapsed_time(g1) / n_b)
+        if pgr is not None:
             pgr.close()
         bflops = 10.0 * N * N * D * BH
-        my_frac = info.my_work_pairs / info.total_work_pairs
+        my_frac = pb.info().my_work_pairs / pb.info().total_work_pairs
         bwd = {"metric": "exact-attn backward TFLOP/s (algorithmic 10*N^2*D*B*H)",
                "value": bflops / (b_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": b_ms,
                "steps": n_b,
@@ -333,29 +517,62 @@ def main():
                        + (" ; PeerGradReduce sum over NVLink" if world > 1 else "")}
         del bws, dq, dk, dv, do
 
-    # ---- end-to-end through the public C-ABI call with HOST buffers (streamed mode: per-task H2D
-    #      of the needed segments double-buffered against compute, O / lse D2H) ----
+    # ---- end-to-end through the public C-ABI call with HOST buffers: streamed mode (per-task H2D
+    #      of the needed segments double-buffered against compute); at N > 1 every rank stages
+    #      only its own tasks' segments from one node-shared pinned copy, then the exchange, then
+    #      the D2H of its owned O / lse rows ----
     e2e = None
-    if not args.no_e2e and world == 1:
-        del ws
-        torch.cuda.empty_cache()
-        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
-        ho = torch.empty(out.shape, dtype=out.dtype).pin_memory()
-        hl = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
-        sdesc = dict(desc_kw, qkv_loc="host", out_loc="host")
+    if not args.no_e2e:
+        if px is not None:
+            px.close()
+            px = None
+        if resident:
+            del ws
+            q = k = v = None
+            torch.cuda.empty_cache()
+        if host_qkv is None:
+            host_qkv = make_host_qkv()
+        hq, hk, hv = host_qkv
+        sdesc = dict(desc_kw, qkv_loc="host", out_loc="host", schedule="uniform")
         ps = cqs.cqs_plan(**sdesc)
         sdev, shost = cqs.cqs_forward_workspace_size(ps)
-        sws = torch.empty(max(sdev, 256), dtype=torch.uint8, device=dev)
+        if resident or sdev != dev_bytes:
+            ws = None
+            torch.cuda.empty_cache()
+            sws = torch.empty(max(sdev, 256), dtype=torch.uint8, device=dev)
+        else:
+            sws = ws
         shws = torch.empty(max(shost, 256), dtype=torch.uint8).pin_memory() if shost else None
+        if world == 1:
+            ho = hout if hout is not None else torch.empty(B, H, N, D, dtype=dt).pin_memory()
+            hl = hlse if hlse is not None else torch.empty(B, H, N, dtype=torch.float32).pin_memory()
+        else:
+            ho = torch.empty(B, H, my_rows, D, dtype=dt).pin_memory()
+            hl = torch.empty(B, H, my_rows, dtype=torch.float32).pin_memory()
+        spx = cdist.PeerExchange(ps, sws) if (world > 1 and args.exchange == "p2p") else None
         h2d = d2h = 0
 
         def e2e_step():
             p = cqs.cqs_plan(**sdesc)
-            return cqs.cqs_attention_forward(p, hq, hk, hv, ho, hl, 0.0, 0, sws, shws, stream,
-                                             stats=True)
+            if world == 1:
+                return cqs.cqs_attention_forward(p, hq, hk, hv, ho, hl, 0.0, 0, sws, shws, stream,
+                                                 stats=True)
+            st = cqs.cqs_attention_forward(p, hq, hk, hv, None, None, 0.0, 0, sws, None, stream,
+                                           stats=True)
+            if spx is not None:
+                spx.merge(out, lse, stream)
+            else:
+                acc_o, acc_l = cdist.partial_accumulator(ps, sws)
+                ro, rl, off, pr0 = cdist.exchange_partials(ps, acc_o, acc_l)
+                cdist.merge_received(ps, ro, rl, off, pr0, out, lse, stream)
+            ho.copy_(out, non_blocking=True)
+            hl.copy_(lse, non_blocking=True)
+            st.bytes_d2h = ho.numel() * ho.element_size() + hl.numel() * 4
+            return st
 
         e2e_step()
         torch.cuda.synchronize()
+        barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n_e2e = max(1, min(args.steps, 3))
         f0.record(stream)
@@ -364,7 +581,10 @@ def main():
             h2d, d2h = st.bytes_h2d, st.bytes_d2h
         f1.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = f0.elapsed_time(f1) / n_e2e
+        barrier()
+        e2e_ms = max_over_ranks(f0.elapsed_time(f1) / n_e2e)
+        if spx is not None:
+            spx.close()
         # host link reference (SURVEY §8d "Streaming: host link"): pinned 1 GiB, best of 3
         link = {}
         hb = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
@@ -384,45 +604,19 @@ def main():
         e2e = {"value": flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "host_link": link,
                "h2d_achieved_gbs": h2d / (e2e_ms * 1e-3) / 1e9,
                "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "cqs_attention_forward with Q/K/V/O/lse in pinned host memory (streamed)",
+               "path": ("cqs_attention_forward with Q/K/V/O/lse in pinned host memory (streamed)"
+                        if world == 1 else
+                        "per rank: cqs_attention_forward streamed (its tasks' segments H2D from "
+                        "a node-shared pinned Q/K/V), exchange, owned O / lse rows D2H"),
                "acc_depth": ps.info().acc_depth, "stage_buffers": ps.info().n_stage_buffers}
-        del hq, hk, hv, ho, hl, sws, shws
+        if world > 1:
+            e2e["note"] = "h2d/d2h bytes are rank %d's; every rank moves its own share" % rank
+        del sws, shws
+        torch.cuda.empty_cache()
 
-    # ---- end-to-end at N > 1 (streamed mode is single-GPU): every step H2D-copies the full Q/K/V
-    #      from pinned host memory to each rank (tasks read arbitrary rows), runs the plan +
-    #      task-sharded forward + exchange, and D2H-copies the rank's owned rows of O / lse ----
-    if not args.no_e2e and world > 1:
-        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
-        ho = torch.empty((B, H, my_rows, D), dtype=out.dtype).pin_memory()
-        hl = torch.empty((B, H, my_rows), dtype=lse.dtype).pin_memory()
-
-        def e2e_step():
-            for dt_, ht in ((q, hq), (k, hk), (v, hv)):
-                dt_.copy_(ht, non_blocking=True)
-            step(False)
-            ho.copy_(out[:, :, row0:row0 + my_rows], non_blocking=True)
-            hl.copy_(lse[:, :, row0:row0 + my_rows], non_blocking=True)
-
-        e2e_step()
-        torch.cuda.synchronize()
-        dist.barrier()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n_e2e = max(1, min(args.steps, 3))
-        f0.record(stream)
-        for _ in range(n_e2e):
-            e2e_step()
-        f1.record(stream)
-        torch.cuda.synchronize()
-        t = torch.tensor([f0.elapsed_time(f1) / n_e2e],
-                         device=dev if dist.get_backend() == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-        e2e = {"value": flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": 3 * q.numel() * q.element_size(),
-               "d2h_bytes_per_step": ho.numel() * ho.element_size() + hl.numel() * 4,
-               "path": "per rank: full Q/K/V H2D from pinned host, cqs_attention_forward (resident, "
-                       "task-sharded) + exchange, owned O / lse rows D2H"}
-        del hq, hk, hv, ho, hl
+    budget = None
+    if world == 1 and not args.no_budget:
+        budget = budget_run(dev, local)
 
     if rank != 0:
         dist.destroy_process_group()
@@ -432,13 +626,14 @@ def main():
     traffic = ncu_traffic(kname)
     peak = peaks.get("bf16_tflops", 1645.9)
     value = flops / (ms * 1e-3) / 1e12
-    # attention-kernel-only rate: this rank's algorithmic FLOPs / summed kernel durations (CUDA events)
+    # attention-kernel-only rate: rank 0's algorithmic FLOPs / summed kernel durations (CUDA events)
     attn_tf = (flops * info.my_work_pairs / info.total_work_pairs) / (attn_ms / args.steps * 1e-3) / 1e12 \
         if attn_ms else None
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and N <= (1 << 20):
         tf, rows, thr, secs = cpu_oracle_sample(cfg)
-        cpu = {"value": tf, "unit": "TFLOP/s", "cores": thr, "kind": "oracle",
+        cpu = {"value": tf, "unit": "TFLOP/s", "cores": thr, "cpu_model": lscpu_model(),
+               "kind": "oracle",
                "sample": "%d query rows of head 0 x all %d keys, fp64 NumPy blockwise dense, %.1f s"
                          % (rows, N, secs)}
     line = {
@@ -446,9 +641,13 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
         "config": {"workload": cfg["desc"], "N": N, "B": B, "H": H, "D": D, "depth": info.depth,
-                   "max_depth": info.max_depth, "schedule": cfg.get("schedule", "uniform"),
-                   "tasks": info.n_tasks, "my_work_frac": info.my_work_pairs / info.total_work_pairs, "l2": "inputs %.1f GB >> 126 MB L2 (no flush needed)"
-                   % (3 * q.numel() * q.element_size() / 1e9),
+                   "max_depth": info.max_depth, "schedule": desc_kw["schedule"],
+                   "shard": desc_kw["shard"] if world > 1 else None,
+                   "inputs": "resident in HBM" if resident else
+                             "pinned host memory (streamed: the plan does not fit HBM resident)",
+                   "tasks": info.n_tasks, "my_work_frac": info.my_work_pairs / info.total_work_pairs,
+                   "l2": "inputs %.1f GB >> 126 MB L2 (no flush needed)"
+                   % (3 * N * BH * D * (2 if bf else 4) / 1e9),
                    "parallelism": "task-sharded x%d" % world,
                    "exchange": args.exchange if world > 1 else None},
         "tokens_per_s": N * B / (ms * 1e-3),
@@ -460,12 +659,15 @@ def main():
                      "kernel": kname, "peak_source": peak_src + " bf16_tflops (burst)",
                      "frac_of_sustained": (attn_tf / peaks.get("bf16_tflops_sustained", peak))
                      if attn_tf else None,
-                     "flops_per_launch": flops / max(1, info.my_tasks),
-                     "launches_per_step": info.my_tasks},
+                     "flops_per_launch": flops * info.my_work_pairs / info.total_work_pairs
+                     / max(1, info.my_tasks),
+                     "launches_per_step": info.my_tasks,
+                     "slowest_rank_kernel_ms_per_step": kern_ms_max},
         "peak_mem": {"predicted_bytes": info.predicted_peak_bytes,
                      "measured_bytes_timed_region": timed_peak,
-                     "note": "all device bytes live during the timed steps (Q/K/V/O/lse + "
-                             "workspace; torch caching-allocator view, no budget set for C2)"},
+                     "note": "rank 0's device bytes live during the timed steps (caller tensors + "
+                             "workspace; torch allocator view); the budgeted run is `budget`"},
+        "budget": budget,
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
         "backward": bwd,
     }

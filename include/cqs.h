@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define CQS_ABI_VERSION 3
+#define CQS_ABI_VERSION 4
 #define CQS_MAX_DEPTH 12   /* N >= 7^depth and N < 2^31 imply depth <= 11 for c = 7           */
 #define CQS_MAX_SEGS 32    /* segments per task; observed <= 8 up to depth 11     */
 
@@ -77,10 +77,29 @@ typedef struct {
   const int32_t* level_c;    /* n_level_sets chunk counts, each l(l-1)+1                      */
   const int32_t* level_offsets; /* concatenated offsets, l_t per level, each a difference set
                                    with offsets[0] = 0 (host memory, copied by cqs_plan)    */
+  int32_t shard;             /* world > 1 task assignment (tasks are independent, so
+                                any assignment is exact).  CQS_SHARD_LPT: largest work first to
+                                the least-loaded rank (best balance).  CQS_SHARD_CONTIGUOUS:
+                                ranks take consecutive runs of the lexicographic (DFS) task order
+                                split at equal work, so a rank's tasks share subtrees and touch
+                                fewer rows — its accumulator (which holds only the rows its tasks
+                                touch, see cqs_partial_runs) shrinks, e.g. to <= 70% of N at
+                                C4 / world 8.  Ignored when world = 1.                          */
+  int32_t reserved0;         /* must be 0                                                       */
+  const int64_t* exec_order; /* NULL, or a permutation of [0, n_tasks) (host memory, copied): the
+                                rank runs its tasks in this relative order instead of the
+                                lexicographic one.  Any order is exact (the LSE merge is
+                                associative and commutative, Eq. 3) up to fp rounding.
+                                CQS_E_INVALID if not a permutation of the planned task count.   */
+  int64_t n_exec_order;
 } cqs_plan_desc;
 
 #define CQS_SCHED_UNIFORM 0
 #define CQS_SCHED_HYBRID 1
+#define CQS_SHARD_LPT 0
+#define CQS_SHARD_CONTIGUOUS 1
+/* Rank-local accumulators (world > 1) are kept in blocks of this many consecutive rows. */
+#define CQS_ACC_BLOCK_ROWS 256
 
 typedef struct cqs_plan_s cqs_plan_t; /* opaque, library-owned, immutable */
 
@@ -98,7 +117,13 @@ typedef struct {
   uint64_t my_work_pairs;
   uint64_t dev_workspace_bytes;  /* = cqs_forward_workspace_size(...).dev                      */
   uint64_t host_workspace_bytes; /* pinned host bytes (streamed mode)                          */
-  uint64_t predicted_peak_bytes; /* memory model M_dev: caller device tensors + dev workspace   */
+  uint64_t predicted_peak_bytes; /* memory model M_dev: caller device tensors + dev workspace
+                                    (each tensor at the allocator's 512-byte granularity, R14);
+                                    world > 1: this rank's bytes (the depth is chosen so that every
+                                    rank fits the budget)                                       */
+  int64_t acc_rows;              /* rows of this rank's fp32 accumulator (N when world = 1; the
+                                    touched blocks of CQS_ACC_BLOCK_ROWS rows when world > 1)   */
+  int64_t shard_rows;            /* world > 1: rows of this rank's output shard (cqs_shard_rows) */
 } cqs_plan_info_t;
 
 typedef struct {
@@ -149,7 +174,10 @@ cqs_status cqs_memory_model(const cqs_plan_desc* desc, int32_t depth, int32_t ac
 typedef struct {
   double ms_plan, ms_h2d, ms_attn, ms_merge, ms_exchange, ms_total; /* filled when stats != NULL
                                                                        (host wall clock, syncs)  */
-  uint64_t bytes_h2d, bytes_d2h, bytes_exchanged, peak_dev_bytes;
+  uint64_t bytes_h2d, bytes_d2h, bytes_exchanged;
+  uint64_t predicted_peak_bytes;   /* the plan's memory-model prediction (not a measurement: the
+                                      library allocates nothing, the caller measures — see
+                                      tests/test_gpu_memory.py and bench.py "budget")            */
   int64_t tasks_run, tasks_skipped, kernel_launches;
 } cqs_stats;
 
@@ -177,8 +205,42 @@ cqs_status cqs_attention_forward(const cqs_plan_t* plan, const void* q, const vo
                                  void* stream /* cudaStream_t */, cqs_stats* stats);
 
 /* Pointers to the fp32 partial accumulator inside dev_ws after a world > 1 forward:
- * acc_o [N][B*H][D], acc_lse [N][B*H] (natural log; -inf = no contribution yet). */
+ * acc_o [acc_rows][B*H][D], acc_lse [acc_rows][B*H] (natural log; -inf = no contribution yet),
+ * acc_rows from cqs_plan_info.  Row layout: see cqs_partial_runs. */
 cqs_status cqs_partial_view(const cqs_plan_t* plan, void* dev_ws, float** acc_o, float** acc_lse);
+
+/* Which global rows rank `src_rank`'s accumulator holds (world > 1; every rank builds the same plan,
+ * so any rank can ask about any other).  A rank's accumulator keeps the blocks of
+ * CQS_ACC_BLOCK_ROWS consecutive rows that contain a query row of one of its tasks (rows of an
+ * active query segment), packed in increasing global order: global row g of a held block sits at
+ * local row slot(g / CQS_ACC_BLOCK_ROWS) * CQS_ACC_BLOCK_ROWS + g % CQS_ACC_BLOCK_ROWS.  With world
+ * = 1 the accumulator is the identity over all N rows.
+ *   runs  : receives up to max_runs triplets (global_start, len, local_row) — maximal runs of held
+ *           rows inside [row0, row0 + rows), ascending (local rows are consecutive inside a run
+ *           and across runs);
+ *   n_runs: receives the number of runs (also when runs is NULL / max_runs too small: then
+ *           CQS_OK with runs untouched if runs == NULL, CQS_E_INVALID otherwise).
+ * Errors: CQS_E_INVALID (bad rank or range). */
+cqs_status cqs_partial_runs(const cqs_plan_t* plan, int32_t src_rank, int64_t row0, int64_t rows,
+                            int64_t* runs, int64_t max_runs, int64_t* n_runs);
+
+/* The single exchange step of a world > 1 forward (Eq. 3): this plan's rank
+ * owns rows [row0, row0 + shard_rows) (cqs_shard_rows) and merges, for each of them, the partial
+ * rows of every rank whose accumulator holds it (cqs_partial_runs), then writes the final O / lse.
+ *   part_o / part_lse : HOST arrays of `world` device pointers (peer memory from cqs_ipc_open, or
+ *                       received all-to-all buffers); rank r's local accumulator row x is read at
+ *                       part_o[r] + (x - part_row0[r]) * B*H*D and part_lse[r] + (x - part_row0[r]) *
+ *                       B*H (part_row0 HOST array; 0 for a whole mapped accumulator, the first
+ *                       local row sent for an all-to-all buffer).
+ *   out               : device [B,H,shard_rows,D] of desc.out_dtype, element strides out_strides
+ *                       (stride D = 1); row 0 = global row row0.
+ *   lse_out           : nullable, device fp32 [B,H,shard_rows] contiguous.
+ * One merge kernel per maximal run of rows held by the same set of ranks.  Errors: CQS_E_INVALID
+ * (world = 1, NULL pointers), CQS_E_CUDA. */
+cqs_status cqs_exchange_merge(const cqs_plan_t* plan, const float* const* part_o,
+                              const float* const* part_lse, const int64_t* part_row0, void* out,
+                              const int64_t out_strides[4], float* lse_out,
+                              void* stream /* cudaStream_t */);
 
 /* ---------------------------------------------------------------------------------------------
  * Backward (Algorithm 2; gradient derivation Appendix D).

@@ -25,6 +25,10 @@ def _a256(x):
     return (x + 255) // 256 * 256
 
 
+def _a512(x):
+    return (x + 511) // 512 * 512
+
+
 def leaf_staged_rows(N, c, I, k):
     """Largest number of rows any non-empty leaf must stage: segments that are a query or key of a
     kept block.  Uses the literal Alg. 3 entry and its mask groups."""
@@ -62,11 +66,13 @@ def workspace_bytes(N, BH, D, e_in, streamed, out_host, staged_rows, acc_rows, n
 
 
 def device_bytes(N, B, H, D, e_in, e_out, streamed, out_host, staged_rows, acc_rows, nbuf):
+    """Each tensor at the caching allocator's 512-byte granularity (R14)."""
     BH = B * H
-    caller = 0 if streamed else 3 * BH * N * D * e_in
+    caller = 0 if streamed else 3 * _a512(BH * N * D * e_in)
     if not out_host:
-        caller += BH * N * D * e_out + 4 * BH * N
-    return caller + workspace_bytes(N, BH, D, e_in, streamed, out_host, staged_rows, acc_rows, nbuf)
+        caller += _a512(BH * N * D * e_out) + _a512(4 * BH * N)
+    return caller + _a512(workspace_bytes(N, BH, D, e_in, streamed, out_host, staged_rows,
+                                          acc_rows, nbuf))
 
 
 def choose(N, B, H, D, e_in, e_out, streamed, out_host, budget, c=7, I=(0, 1, 3), depth=None,
@@ -108,4 +114,4 @@ def backward_workspace_bytes(N, BH, D, streamed=False, staged_rows=0, nbuf=0):
         b += nbuf * 4 * _a256(BH * staged_rows * D * 2)
         F = min(max((64 << 20) // (BH * D * 4), 256), 65536, N)
         b += 2 * (_a256(F * BH * D * 4) + _a256(F * BH * 4))
-    return b
+    return _a512(b)

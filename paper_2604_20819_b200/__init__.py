@@ -24,6 +24,8 @@ CQS_OK, CQS_E_VERIFY, CQS_E_INFEASIBLE, CQS_E_INVALID, CQS_E_CUDA, CQS_E_NCCL, C
 CQS_F32, CQS_BF16 = 0, 1
 CQS_LOC_DEVICE, CQS_LOC_PINNED_HOST = 0, 1
 CQS_SCHED_UNIFORM, CQS_SCHED_HYBRID = 0, 1
+CQS_SHARD_LPT, CQS_SHARD_CONTIGUOUS = 0, 1
+CQS_ACC_BLOCK_ROWS = 256
 CQS_MAX_DEPTH, CQS_MAX_SEGS = 12, 32
 STATUS_NAMES = {0: "CQS_OK", 1: "CQS_E_VERIFY", 2: "CQS_E_INFEASIBLE", 3: "CQS_E_INVALID",
                 4: "CQS_E_CUDA", 5: "CQS_E_NCCL", 6: "CQS_E_OOM", 7: "CQS_E_UNSUPPORTED"}
@@ -34,7 +36,8 @@ ABI_SYMBOLS = ("cqs_plan", "cqs_plan_info", "cqs_plan_task", "cqs_plan_serialize
                "cqs_attention_forward", "cqs_partial_view", "cqs_shard_rows", "cqs_merge",
                "cqs_ipc_handle", "cqs_ipc_open", "cqs_ipc_close", "cqs_last_error",
                "cqs_abi_version", "cqs_backward_workspace_size", "cqs_attention_backward",
-               "cqs_backward_partial_view", "cqs_reduce_sum")
+               "cqs_backward_partial_view", "cqs_reduce_sum", "cqs_partial_runs",
+               "cqs_exchange_merge")
 
 
 class CqsError(RuntimeError):
@@ -50,7 +53,9 @@ class PlanDesc(C.Structure):
                 ("out_dtype", C.c_int), ("qkv_loc", C.c_int), ("out_loc", C.c_int),
                 ("world", C.c_int32), ("rank", C.c_int32), ("schedule", C.c_int32),
                 ("n_level_sets", C.c_int32), ("level_c", C.POINTER(C.c_int32)),
-                ("level_offsets", C.POINTER(C.c_int32))]
+                ("level_offsets", C.POINTER(C.c_int32)), ("shard", C.c_int32),
+                ("reserved0", C.c_int32), ("exec_order", C.POINTER(C.c_int64)),
+                ("n_exec_order", C.c_int64)]
 
 
 class PlanInfo(C.Structure):
@@ -59,7 +64,8 @@ class PlanInfo(C.Structure):
                 ("max_task_rows", C.c_int64), ("max_staged_rows", C.c_int64),
                 ("total_work_pairs", C.c_uint64), ("my_tasks", C.c_int64),
                 ("my_work_pairs", C.c_uint64), ("dev_workspace_bytes", C.c_uint64),
-                ("host_workspace_bytes", C.c_uint64), ("predicted_peak_bytes", C.c_uint64)]
+                ("host_workspace_bytes", C.c_uint64), ("predicted_peak_bytes", C.c_uint64),
+                ("acc_rows", C.c_int64), ("shard_rows", C.c_int64)]
 
 
 class Task(C.Structure):
@@ -75,7 +81,7 @@ class Stats(C.Structure):
     _fields_ = [("ms_plan", C.c_double), ("ms_h2d", C.c_double), ("ms_attn", C.c_double),
                 ("ms_merge", C.c_double), ("ms_exchange", C.c_double), ("ms_total", C.c_double),
                 ("bytes_h2d", C.c_uint64), ("bytes_d2h", C.c_uint64),
-                ("bytes_exchanged", C.c_uint64), ("peak_dev_bytes", C.c_uint64),
+                ("bytes_exchanged", C.c_uint64), ("predicted_peak_bytes", C.c_uint64),
                 ("tasks_run", C.c_int64), ("tasks_skipped", C.c_int64),
                 ("kernel_launches", C.c_int64)]
 
@@ -116,6 +122,10 @@ def lib():
         L.cqs_backward_partial_view.argtypes = [P, P, C.POINTER(P), C.POINTER(P), C.POINTER(P)]
         L.cqs_reduce_sum.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                      C.POINTER(P), P, C.c_int, C.POINTER(C.c_int64), C.c_int64, P]
+        L.cqs_partial_runs.argtypes = [P, C.c_int32, C.c_int64, C.c_int64, C.POINTER(C.c_int64),
+                                       C.c_int64, C.POINTER(C.c_int64)]
+        L.cqs_exchange_merge.argtypes = [P, C.POINTER(P), C.POINTER(P), C.POINTER(C.c_int64), P,
+                                         C.POINTER(C.c_int64), P, P]
         L.cqs_ipc_handle.argtypes = [P, P, C.POINTER(C.c_uint64)]
         L.cqs_ipc_open.argtypes = [P, C.POINTER(P)]
         L.cqs_ipc_close.argtypes = [P]
@@ -151,9 +161,10 @@ def _loc_code(x):
 
 def make_desc(N, B, H, D, depth=1, budget_bytes=0, in_dtype="bf16", out_dtype=None,
               qkv_loc="device", out_loc=None, world=1, rank=0, c=7, offsets=(0, 1, 3),
-              schedule="uniform", levels=None):
+              schedule="uniform", levels=None, shard="lpt", exec_order=None):
     """levels: optional [(c_t, offsets_t), ...] interest sets for divide levels 0, 1, ...
-    (deeper levels use (c, offsets))."""
+    (deeper levels use (c, offsets)).  shard: "lpt" | "contiguous" (world > 1 assignment).
+    exec_order: optional permutation of the task indices (this rank's execution order)."""
     offs = (C.c_int32 * len(offsets))(*offsets)
     levels = list(levels or [])
     lc = (C.c_int32 * max(len(levels), 1))(*[int(c_t) for c_t, _ in levels])
@@ -167,8 +178,15 @@ def make_desc(N, B, H, D, depth=1, budget_bytes=0, in_dtype="bf16", out_dtype=No
                  world=world, rank=rank,
                  schedule={"uniform": CQS_SCHED_UNIFORM, "hybrid": CQS_SCHED_HYBRID}.get(
                      schedule, schedule),
-                 n_level_sets=len(levels), level_c=lc, level_offsets=lo)
-    d._offs = (offs, lc, lo)  # keep alive
+                 n_level_sets=len(levels), level_c=lc, level_offsets=lo,
+                 shard={"lpt": CQS_SHARD_LPT, "contiguous": CQS_SHARD_CONTIGUOUS}.get(shard, shard),
+                 reserved0=0)
+    eo = None
+    if exec_order is not None:
+        eo = (C.c_int64 * max(len(exec_order), 1))(*[int(x) for x in exec_order])
+        d.exec_order = C.cast(eo, C.POINTER(C.c_int64))
+        d.n_exec_order = len(exec_order)
+    d._offs = (offs, lc, lo, eo)  # keep alive
     return d
 
 
@@ -319,6 +337,30 @@ def cqs_partial_view(plan: Plan, dev_ws):
     o, l_ = C.c_void_p(), C.c_void_p()
     _check(lib().cqs_partial_view(plan.handle, _ptr(dev_ws), C.byref(o), C.byref(l_)))
     return o.value, l_.value
+
+
+def cqs_partial_runs(plan: Plan, src_rank, row0, rows):
+    """[(global_start, len, local_row)] of the rows of [row0, row0+rows) that rank src_rank's
+    accumulator holds (world > 1: held blocks of CQS_ACC_BLOCK_ROWS rows; world 1: identity)."""
+    n = C.c_int64()
+    _check(lib().cqs_partial_runs(plan.handle, int(src_rank), int(row0), int(rows), None, 0,
+                                  C.byref(n)))
+    buf = (C.c_int64 * max(3 * n.value, 1))()
+    _check(lib().cqs_partial_runs(plan.handle, int(src_rank), int(row0), int(rows), buf, n.value,
+                                  C.byref(n)))
+    return [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(n.value)]
+
+
+def cqs_exchange_merge(plan: Plan, part_o, part_lse, part_row0, out, lse_out=None, stream=None):
+    """The world > 1 exchange merge of this plan's rank: part_o / part_lse = one device address
+    (int) or fp32 tensor per rank, part_row0 = the local accumulator row each pointer's row 0 is;
+    out: device [B,H,shard_rows,D] (the plan's out dtype), lse_out: device fp32 [B,H,shard_rows]."""
+    n = len(part_o)
+    po = (C.c_void_p * n)(*[_addr(t) for t in part_o])
+    pl = (C.c_void_p * n)(*[_addr(t) for t in part_lse])
+    pr = (C.c_int64 * n)(*[int(x) for x in part_row0])
+    _check(lib().cqs_exchange_merge(plan.handle, po, pl, pr, _ptr(out), _i64x4(out.stride()),
+                                    _ptr(lse_out), _stream_ptr(stream)))
 
 
 def cqs_shard_rows(N, world, rank):

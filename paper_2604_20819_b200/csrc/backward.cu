@@ -68,6 +68,7 @@ static BwdLayout bwd_layout(const cqs_plan_t* p, int nbuf) {
     L.chunk_bytes = L.chunk_lse + align256(uint64_t(L.F) * BH * 4);
     L.total = L.chunk + 2 * L.chunk_bytes;
   }
+  L.total = align512(L.total);   // the caller's allocator granularity (R14)
   return L;
 }
 
@@ -241,7 +242,7 @@ extern "C" cqs_status cqs_attention_backward(const cqs_plan_t* p, const void* q,
     stats->tasks_run = run;
     stats->tasks_skipped = int64_t(p->tasks.size()) - run;
     stats->kernel_launches = launches;
-    stats->peak_dev_bytes = L.total;
+    stats->predicted_peak_bytes = L.total;
   }
   return CQS_OK;
 }
@@ -437,7 +438,7 @@ cqs_status backward_streamed(const cqs_plan_t* p, const BwdLayout& L, const void
     stats->tasks_run = run;
     stats->tasks_skipped = int64_t(p->tasks.size()) - run;
     stats->kernel_launches = launches;
-    stats->peak_dev_bytes = L.total;
+    stats->predicted_peak_bytes = L.total;
   }
   return CQS_OK;
 }

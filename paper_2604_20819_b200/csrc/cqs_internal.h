@@ -57,7 +57,19 @@ struct cqs_plan_s {
   std::vector<cqs::Task> tasks;      // c^depth, lexicographic
   std::vector<cqs::Seg> segs;        // CSR storage of task segments
   std::vector<int64_t> my_order;     // non-empty tasks of `rank`, execution order
+  // world > 1: rank-local accumulator = the blocks of CQS_ACC_BLOCK_ROWS rows holding a query row
+  // of this rank's tasks, packed in increasing global order; acc_slot[block] = local block or -1.
+  // Empty when world = 1 (identity over N rows).
+  std::vector<int32_t> acc_slot;
+  int64_t shard_rows = 0;            // world > 1: rows of this rank's output shard
   int64_t n_empty = 0, max_task_rows = 0, max_staged_rows = 0, max_acc_rows = 0;
+  // accumulator row of global row g (segments never straddle an unheld block: all rows of an
+  // active query segment are held, so a segment's accumulator rows are consecutive)
+  int64_t acc_row(int64_t g) const {
+    if (acc_slot.empty()) return g;
+    const int32_t s = acc_slot[size_t(g / CQS_ACC_BLOCK_ROWS)];
+    return s < 0 ? -1 : int64_t(s) * CQS_ACC_BLOCK_ROWS + g % CQS_ACC_BLOCK_ROWS;
+  }
   uint64_t total_work = 0, my_work = 0;
   uint64_t dev_ws = 0, host_ws = 0, predicted_peak = 0;
 };
@@ -67,9 +79,15 @@ namespace cqs {
 struct MemModel {
   uint64_t caller_dev, dev_ws, host_ws;
 };
+// out_rows: rows of O / lse the call's caller holds on the device (N; world > 1: the output shard,
+// which the exchange writes on the device whatever out_loc says).
 MemModel memory_model(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_rows,
-                      int32_t n_stage_buffers);
+                      int32_t n_stage_buffers, int64_t out_rows);
+// Held accumulator blocks (CQS_ACC_BLOCK_ROWS rows) of rank r under the current Task::rank values.
+void held_blocks(const std::vector<Task>& tasks, const std::vector<Seg>& segs, int64_t N,
+                 int32_t r, std::vector<uint8_t>& held);
 uint64_t align256(uint64_t x);
+uint64_t align512(uint64_t x);
 // Section offsets of the device workspace (forward.cu must follow memory_model exactly).
 struct WsLayout {
   uint64_t acc_o, acc_lse, stage, stage_bytes_per_buf, flush, total;

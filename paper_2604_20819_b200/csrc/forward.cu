@@ -120,9 +120,9 @@ using namespace cqs;
 extern "C" cqs_status cqs_partial_view(const cqs_plan_t* p, void* dev_ws, float** acc_o,
                                        float** acc_lse) {
   if (!p || !dev_ws || !acc_o || !acc_lse) return fail(CQS_E_INVALID, "NULL argument");
-  if (p->desc.qkv_loc != CQS_LOC_DEVICE)
-    return fail(CQS_E_UNSUPPORTED, "partial view exists for resident plans only");
-  const WsLayout L = ws_layout(p->desc, 0, p->desc.N, 0);
+  if (p->desc.world == 1 && p->desc.qkv_loc != CQS_LOC_DEVICE)
+    return fail(CQS_E_UNSUPPORTED, "partial view: resident or world > 1 plans only");
+  const WsLayout L = ws_layout(p->desc, p->max_staged_rows, p->max_acc_rows, p->n_stage_buffers);
   *acc_o = reinterpret_cast<float*>(static_cast<uint8_t*>(dev_ws) + L.acc_o);
   *acc_lse = reinterpret_cast<float*>(static_cast<uint8_t*>(dev_ws) + L.acc_lse);
   return CQS_OK;
@@ -162,7 +162,7 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
   if (!qkv_strides || qkv_strides[3] != 1)
     return fail(CQS_E_INVALID, "qkv strides: stride(D) must be 1");
   const int BH = d.B * d.H;
-  const WsLayout L = ws_layout(d, 0, d.N, 0);
+  const WsLayout L = ws_layout(d, 0, p->max_acc_rows, 0);
   float* acc_o = reinterpret_cast<float*>(ws + L.acc_o);
   float* acc_lse = reinterpret_cast<float*>(ws + L.acc_lse);
   int64_t launches = 0;
@@ -176,7 +176,7 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
     evs.push_back(ev);
   };
   mark();
-  cudaError_t e = launch_fill(acc_lse, d.N * BH, -INFINITY, st);
+  cudaError_t e = launch_fill(acc_lse, p->max_acc_rows * BH, -INFINITY, st);
   mark();
   ++launches;
   if (e != cudaSuccess) return fail(CQS_E_CUDA, cudaGetErrorString(e));
@@ -197,7 +197,8 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
   for (int64_t ti : p->my_order) {
     const Task& T = p->tasks[size_t(ti)];
     auto seg_start = [&](int a) { return p->segs[size_t(T.seg_off + a)].start; };
-    build_task_params(p, T, rows_per_item, seg_start, seg_start, tp);
+    auto seg_acc = [&](int a) { return p->acc_row(p->segs[size_t(T.seg_off + a)].start); };
+    build_task_params(p, T, rows_per_item, seg_start, seg_acc, tp);
     mark();
     if (d.in_dtype == CQS_BF16)
       e = launch_attn_bf16(d.D, maps, tp, acc_o, acc_lse, scale, st);
@@ -236,7 +237,7 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
     stats->tasks_run = run;
     stats->tasks_skipped = int64_t(p->tasks.size()) - run;
     stats->kernel_launches = launches;
-    stats->peak_dev_bytes = p->predicted_peak;
+    stats->predicted_peak_bytes = p->predicted_peak;
   }
   return CQS_OK;
 }

@@ -28,6 +28,7 @@ cqs_status fail(cqs_status st, const std::string& msg) {
 }
 
 uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
+uint64_t align512(uint64_t x) { return (x + 511) & ~uint64_t(511); }
 
 static int64_t elem_size(cqs_dtype t) { return t == CQS_BF16 ? 2 : 4; }
 
@@ -48,7 +49,9 @@ WsLayout ws_layout(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_rows
     off += uint64_t(n_stage_buffers) * w.stage_bytes_per_buf;
   }
   w.flush = off;
-  if (d.qkv_loc == CQS_LOC_PINNED_HOST || d.out_loc == CQS_LOC_PINNED_HOST) {
+  // flush buffers stage host-tier accumulator chunks and final rows (world = 1 streamed / host
+  // output); a world > 1 call leaves its partials on the device for the exchange
+  if (d.world == 1 && (d.qkv_loc == CQS_LOC_PINNED_HOST || d.out_loc == CQS_LOC_PINNED_HOST)) {
     const uint64_t F = uint64_t(flush_rows(acc_rows, int64_t(BH), int64_t(D)));
     off += 2 * (align256(F * BH * D * 4) + align256(F * BH * 4));
   }
@@ -57,14 +60,19 @@ WsLayout ws_layout(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_rows
 }
 
 MemModel memory_model(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_rows,
-                      int32_t n_stage_buffers) {
-  const uint64_t BH = uint64_t(d.B) * d.H, N = d.N, D = d.D;
+                      int32_t n_stage_buffers, int64_t out_rows) {
+  const uint64_t BH = uint64_t(d.B) * d.H, N = d.N, D = d.D, R = uint64_t(out_rows);
   MemModel m{};
+  // every tensor counted at the caching allocator's 512-byte granularity (R14): a caller that
+  // allocates Q, K, V, O, lse and the workspace as separate torch tensors sees exactly this many
+  // allocated bytes
   m.caller_dev = 0;
-  if (d.qkv_loc == CQS_LOC_DEVICE) m.caller_dev += 3 * BH * N * D * elem_size(d.in_dtype);
-  if (d.out_loc == CQS_LOC_DEVICE) m.caller_dev += BH * N * D * elem_size(d.out_dtype) + 4 * BH * N;
-  m.dev_ws = ws_layout(d, staged_rows, acc_rows, n_stage_buffers).total;
-  m.host_ws = (acc_rows < d.N) ? align256(N * BH * D * 4) + align256(N * BH * 4) : 0;
+  if (d.qkv_loc == CQS_LOC_DEVICE) m.caller_dev += 3 * align512(BH * N * D * elem_size(d.in_dtype));
+  if (d.out_loc == CQS_LOC_DEVICE || d.world > 1)
+    m.caller_dev += align512(BH * R * D * elem_size(d.out_dtype)) + align512(4 * BH * R);
+  m.dev_ws = align512(ws_layout(d, staged_rows, acc_rows, n_stage_buffers).total);
+  // pinned host accumulator of the host tier (world = 1 streamed plans with j > 0)
+  m.host_ws = (d.world == 1 && acc_rows < d.N) ? align256(N * BH * D * 4) + align256(N * BH * 4) : 0;
   return m;
 }
 
@@ -267,6 +275,74 @@ static uint64_t lpt_assign(std::vector<Task>& tasks, int world) {
   return *std::max_element(load.begin(), load.end());
 }
 
+// Contiguous assignment: non-empty tasks in lexicographic (DFS) order; a task goes to the rank
+// whose equal-work interval contains the midpoint of its work on the prefix-sum axis, so rank r
+// takes one consecutive run of tasks (a few neighbouring subtrees).  Returns the makespan.
+static uint64_t contiguous_assign(std::vector<Task>& tasks, int world) {
+  uint64_t total = 0;
+  for (const Task& T : tasks) total += T.work;
+  std::vector<uint64_t> load(size_t(world), 0);
+  uint64_t pre = 0;
+  for (Task& T : tasks) {
+    T.rank = -1;
+    if (T.work == 0) continue;
+    const long double mid = (long double)pre + (long double)T.work / 2;
+    int r = int(mid * world / (long double)total);
+    r = std::min(std::max(r, 0), world - 1);
+    T.rank = r;
+    load[size_t(r)] += T.work;
+    pre += T.work;
+  }
+  return *std::max_element(load.begin(), load.end());
+}
+
+static uint64_t assign_ranks(std::vector<Task>& tasks, const cqs_plan_desc& d) {
+  if (d.world > 1 && d.shard == CQS_SHARD_CONTIGUOUS) return contiguous_assign(tasks, d.world);
+  return lpt_assign(tasks, d.world);
+}
+
+void held_blocks(const std::vector<Task>& tasks, const std::vector<Seg>& segs, int64_t N,
+                 int32_t r, std::vector<uint8_t>& held) {
+  const int64_t G = CQS_ACC_BLOCK_ROWS;
+  held.assign(size_t((N + G - 1) / G), 0);
+  for (const Task& T : tasks) {
+    if (T.rank != r) continue;
+    for (int a = 0; a < T.nseg; ++a) {
+      if (!T.kept[a]) continue;                          // not an active query segment
+      const Seg& sg = segs[size_t(T.seg_off + a)];
+      for (int64_t b = sg.start / G; b <= (sg.start + sg.len - 1) / G; ++b) held[size_t(b)] = 1;
+    }
+  }
+}
+
+// Accumulator rows every rank needs (world > 1): held blocks x CQS_ACC_BLOCK_ROWS.
+static std::vector<int64_t> held_rows_per_rank(const std::vector<Task>& tasks,
+                                               const std::vector<Seg>& segs, int64_t N,
+                                               int world) {
+  const int64_t G = CQS_ACC_BLOCK_ROWS, nb = (N + G - 1) / G;
+  std::vector<uint8_t> held(size_t(nb) * size_t(world), 0);
+  for (const Task& T : tasks) {
+    if (T.rank < 0) continue;
+    uint8_t* h = held.data() + size_t(T.rank) * size_t(nb);
+    for (int a = 0; a < T.nseg; ++a) {
+      if (!T.kept[a]) continue;
+      const Seg& sg = segs[size_t(T.seg_off + a)];
+      for (int64_t b = sg.start / G; b <= (sg.start + sg.len - 1) / G; ++b) h[b] = 1;
+    }
+  }
+  std::vector<int64_t> rows(size_t(world), 0);
+  for (int r = 0; r < world; ++r) {
+    int64_t c = 0;
+    for (int64_t b = 0; b < nb; ++b) c += held[size_t(r) * size_t(nb) + size_t(b)];
+    rows[size_t(r)] = c * G;
+  }
+  return rows;
+}
+
+static int64_t shard_rows_of(int64_t N, int world, int rank) {
+  return (N * (rank + 1)) / world - (N * rank) / world;
+}
+
 // Hybrid scheduling (Fig. "schedule" right): leaves at mixed depths.  Starting from the
 // uniform tree, repeatedly replace the heaviest leaf (ties: first in DFS order) by its c children
 // until the LPT makespan is within 1% of total/world.  Any such tree is still an exact
@@ -390,10 +466,31 @@ static cqs_status validate_desc(const cqs_plan_desc* d, Levels& lv) {
     return fail(CQS_E_UNSUPPORTED, "resident Q/K/V require a device output");
   if (d->schedule != CQS_SCHED_UNIFORM && d->schedule != CQS_SCHED_HYBRID)
     return fail(CQS_E_INVALID, "schedule must be CQS_SCHED_UNIFORM or CQS_SCHED_HYBRID");
+  if (d->shard != CQS_SHARD_LPT && d->shard != CQS_SHARD_CONTIGUOUS)
+    return fail(CQS_E_INVALID, "shard must be CQS_SHARD_LPT or CQS_SHARD_CONTIGUOUS");
+  if (d->reserved0 != 0) return fail(CQS_E_INVALID, "reserved0 must be 0");
+  if (d->n_exec_order < 0 || (d->n_exec_order > 0 && !d->exec_order))
+    return fail(CQS_E_INVALID, "exec_order NULL with n_exec_order > 0");
   if (d->schedule == CQS_SCHED_HYBRID && d->qkv_loc == CQS_LOC_PINNED_HOST)
     return fail(CQS_E_UNSUPPORTED, "hybrid schedule: resident plans only (the streamed executor "
                                    "groups uniform subtrees)");
   return CQS_OK;
+}
+
+// Device bytes of a world > 1 call at this leaf set: the task assignment decides each rank's
+// accumulator rows (held blocks); `mine` = this rank's model, return value = the largest over the
+// ranks (the depth / buffer choice must be the same on every rank, and every rank must fit).
+static MemModel sharded_model(const cqs_plan_desc& d, LeafSet& ls, int64_t staged, int nbuf,
+                              MemModel* mine, int64_t* my_acc_rows) {
+  assign_ranks(ls.tasks, d);
+  const std::vector<int64_t> rows = held_rows_per_rank(ls.tasks, ls.segs, d.N, d.world);
+  MemModel worst{};
+  for (int r = 0; r < d.world; ++r) {
+    MemModel m = memory_model(d, staged, rows[size_t(r)], nbuf, shard_rows_of(d.N, d.world, r));
+    if (m.caller_dev + m.dev_ws > worst.caller_dev + worst.dev_ws) worst = m;
+    if (r == d.rank) *mine = m, *my_acc_rows = rows[size_t(r)];
+  }
+  return worst;
 }
 
 cqs_status cqs_memory_model(const cqs_plan_desc* desc, int32_t depth, int32_t acc_depth,
@@ -404,15 +501,27 @@ cqs_status cqs_memory_model(const cqs_plan_desc* desc, int32_t depth, int32_t ac
   if (depth < 0 || depth >= CQS_MAX_DEPTH || acc_depth < 0 || acc_depth > depth ||
       desc->N < lv.tasks(depth))
     return fail(CQS_E_INVALID, "bad depth / acc_depth");
+  const bool streamed = desc->qkv_loc == CQS_LOC_PINNED_HOST, sharded = desc->world > 1;
+  if (sharded && acc_depth != 0)
+    return fail(CQS_E_INVALID, "world > 1 keeps a device accumulator (acc_depth 0)");
   LeafSet ls;
   int64_t staged = desc->N;
-  if (desc->qkv_loc == CQS_LOC_PINNED_HOST) {
+  if (streamed || sharded) {
     if ((st = enumerate_leaves(*desc, lv, depth, ls)) != CQS_OK) return st;
     staged = ls.max_staged;
   }
-  const int64_t acc_rows =
-      desc->qkv_loc == CQS_LOC_PINNED_HOST ? max_node_rows(desc->N, lv, acc_depth) : desc->N;
-  MemModel m = memory_model(*desc, staged, acc_rows, n_stage_buffers);
+  MemModel m;
+  if (sharded) {
+    MemModel mine{};
+    int64_t rows = 0;
+    m = sharded_model(*desc, ls, streamed ? staged : 0, streamed ? n_stage_buffers : 0, &mine,
+                      &rows);
+    m = mine;   // this rank's bytes (cqs_plan chooses by the largest over the ranks)
+  } else {
+    const int64_t acc_rows = streamed ? max_node_rows(desc->N, lv, acc_depth) : desc->N;
+    m = memory_model(*desc, streamed ? staged : 0, acc_rows, streamed ? n_stage_buffers : 0,
+                     desc->N);
+  }
   if (dev_bytes) *dev_bytes = m.caller_dev + m.dev_ws;
   if (host_bytes) *host_bytes = m.host_ws;
   return CQS_OK;
@@ -425,7 +534,7 @@ cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
   cqs_status st = validate_desc(desc, lv);
   if (st != CQS_OK) return st;
   const cqs_plan_desc& d = *desc;
-  const bool streamed = d.qkv_loc == CQS_LOC_PINNED_HOST;
+  const bool streamed = d.qkv_loc == CQS_LOC_PINNED_HOST, sharded = d.world > 1;
   const uint64_t budget = d.budget_bytes;
 
   int max_depth = 0;
@@ -438,24 +547,33 @@ cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
   int chosen = -1, chosen_j = 0, chosen_nbuf = 0;
   int64_t acc_rows = d.N;
   MemModel mm{};
-  if (!streamed) {
-    // resident bytes do not depend on the depth: decide feasibility once, then enumerate only
-    // the chosen depth (the smallest one, or the caller's)
-    mm = memory_model(d, 0, d.N, 0);
-    if (budget != 0 && mm.caller_dev + mm.dev_ws > budget)
+  auto fits = [&](const MemModel& m) { return budget == 0 || m.caller_dev + m.dev_ws <= budget; };
+  if (!streamed && !sharded) {
+    // resident single-GPU bytes do not depend on the depth: decide feasibility once, then
+    // enumerate only the chosen depth (the smallest one, or the caller's)
+    mm = memory_model(d, 0, d.N, 0, d.N);
+    if (!fits(mm))
       return fail(CQS_E_INFEASIBLE, "resident plan exceeds budget_bytes at every depth");
     if ((st = enumerate_leaves(d, lv, k_lo, ls)) != CQS_OK) return st;
     chosen = k_lo;
   }
   for (int k = k_lo; k <= k_hi && chosen < 0; ++k) {
     if ((st = enumerate_leaves(d, lv, k, ls)) != CQS_OK) return st;
+    if (sharded) {
+      // rank-local accumulators (held blocks) on the device; streamed: plus staging buffers
+      for (int nbuf = streamed ? 2 : 0; nbuf >= (streamed ? 1 : 0) && chosen < 0; --nbuf) {
+        MemModel mine{};
+        int64_t rows = 0;
+        const MemModel worst = sharded_model(d, ls, streamed ? ls.max_staged : 0, nbuf, &mine, &rows);
+        if (fits(worst)) chosen = k, chosen_j = 0, chosen_nbuf = nbuf, acc_rows = rows, mm = mine;
+      }
+      continue;
+    }
     for (int nbuf = 2; nbuf >= 1 && chosen < 0; --nbuf)
       for (int j = 0; j <= k && chosen < 0; ++j) {
         const int64_t rows = max_node_rows(d.N, lv, j);
-        MemModel m = memory_model(d, ls.max_staged, rows, nbuf);
-        if (budget == 0 || m.caller_dev + m.dev_ws <= budget) {
-          chosen = k, chosen_j = j, chosen_nbuf = nbuf, acc_rows = rows, mm = m;
-        }
+        MemModel m = memory_model(d, ls.max_staged, rows, nbuf, d.N);
+        if (fits(m)) chosen = k, chosen_j = j, chosen_nbuf = nbuf, acc_rows = rows, mm = m;
       }
   }
   if (chosen < 0)
@@ -471,6 +589,8 @@ cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
   for (auto& I : p->lv.lI) p->level_offsets.insert(p->level_offsets.end(), I.begin(), I.end());
   p->desc.level_c = p->lv.lc.empty() ? nullptr : p->lv.lc.data();
   p->desc.level_offsets = p->level_offsets.empty() ? nullptr : p->level_offsets.data();
+  p->desc.exec_order = nullptr;
+  p->desc.n_exec_order = 0;
   p->depth = chosen;
   p->max_depth = chosen;
   for (const Task& T : ls.tasks) p->max_depth = std::max(p->max_depth, T.depth);
@@ -481,15 +601,46 @@ cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
   p->n_empty = ls.n_empty;
   p->max_task_rows = ls.max_rows;
   p->max_staged_rows = streamed ? ls.max_staged : 0;
-  p->max_acc_rows = acc_rows;
   p->total_work = ls.total_work;
 
-  lpt_assign(p->tasks, d.world);
+  assign_ranks(p->tasks, d);
   for (int64_t i = 0; i < int64_t(p->tasks.size()); ++i)
     if (p->tasks[size_t(i)].rank == d.rank) {
       p->my_order.push_back(i);
       p->my_work += p->tasks[size_t(i)].work;
     }
+  if (d.exec_order) {   // caller's execution order (any order is exact, Eq. 3)
+    const int64_t n = int64_t(p->tasks.size());
+    if (d.n_exec_order != n) {
+      delete p;
+      return fail(CQS_E_INVALID, "exec_order must list all " + std::to_string(n) + " tasks");
+    }
+    std::vector<int64_t> pos(size_t(n), -1);
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t t = d.exec_order[i];
+      if (t < 0 || t >= n || pos[size_t(t)] >= 0) {
+        delete p;
+        return fail(CQS_E_INVALID, "exec_order is not a permutation of the task indices");
+      }
+      pos[size_t(t)] = i;
+    }
+    std::stable_sort(p->my_order.begin(), p->my_order.end(),
+                     [&](int64_t a, int64_t b) { return pos[size_t(a)] < pos[size_t(b)]; });
+  }
+  if (sharded) {
+    // rank-local accumulator: held blocks packed in increasing global order
+    std::vector<uint8_t> held;
+    held_blocks(p->tasks, p->segs, d.N, d.rank, held);
+    p->acc_slot.assign(held.size(), -1);
+    int32_t nb = 0;
+    for (size_t b = 0; b < held.size(); ++b)
+      if (held[b]) p->acc_slot[b] = nb++;
+    acc_rows = int64_t(nb) * CQS_ACC_BLOCK_ROWS;
+    p->shard_rows = shard_rows_of(d.N, d.world, d.rank);
+    // (hybrid refinement may have changed the leaves: re-evaluate this rank's bytes)
+    mm = memory_model(d, p->max_staged_rows, acc_rows, p->n_stage_buffers, p->shard_rows);
+  }
+  p->max_acc_rows = acc_rows;
   p->dev_ws = mm.dev_ws;
   p->host_ws = mm.host_ws;
   p->predicted_peak = mm.caller_dev + mm.dev_ws;
@@ -514,6 +665,8 @@ cqs_status cqs_plan_info(const cqs_plan_t* p, cqs_plan_info_t* info) {
   info->dev_workspace_bytes = p->dev_ws;
   info->host_workspace_bytes = p->host_ws;
   info->predicted_peak_bytes = p->predicted_peak;
+  info->acc_rows = p->max_acc_rows;
+  info->shard_rows = p->desc.world > 1 ? p->shard_rows : 0;
   return CQS_OK;
 }
 

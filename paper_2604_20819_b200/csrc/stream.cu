@@ -73,9 +73,12 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
   const cqs_plan_desc& d = p->desc;
   if (d.out_loc != CQS_LOC_PINNED_HOST)
     return fail(CQS_E_UNSUPPORTED, "streamed Q/K/V require a pinned-host output");
-  if (d.world != 1) return fail(CQS_E_UNSUPPORTED, "streamed mode is single-GPU");
+  // world > 1: this rank stages only its tasks' segments and keeps its partials in the rank-local
+  // device accumulator (held blocks, acc_depth 0); the exchange (cqs_exchange_merge) finalizes
+  const bool sharded = d.world > 1;
   const int64_t N = d.N, D = d.D, BH = int64_t(d.B) * d.H;
-  if (out_strides[0] != int64_t(d.H) * N * D || out_strides[1] != N * D || out_strides[2] != D)
+  if (!sharded && (out_strides[0] != int64_t(d.H) * N * D || out_strides[1] != N * D ||
+                   out_strides[2] != D))
     return fail(CQS_E_INVALID, "streamed mode needs a contiguous [B,H,N,D] output");
   const int64_t e_in = d.in_dtype == CQS_BF16 ? 2 : 4, e_out = d.out_dtype == CQS_BF16 ? 2 : 4;
   const int S = p->n_stage_buffers, j = p->acc_depth;
@@ -194,7 +197,7 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
   // tasks (at depth 1, 4 of the 7 chunks are final before the last task).  fin[ti] = the row
   // ranges whose last task is ti, from a sweep over the active query segments of every task.
   std::vector<std::vector<std::pair<int64_t, int64_t>>> fin;
-  if (j == 0 && nmy > 0) {
+  if (j == 0 && nmy > 0 && !sharded) {
     std::vector<std::pair<int64_t, int64_t>> ev;   // (row, +(ti+1) at start / -(ti+1) at end)
     for (int64_t ti = 0; ti < nmy; ++ti) {
       const Task& T = p->tasks[size_t(p->my_order[size_t(ti)])];
@@ -320,7 +323,7 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
     std::vector<int64_t> node_off(node.size());
     int64_t node_rows = 0;
     for (size_t i = 0; i < node.size(); ++i) node_off[i] = node_rows, node_rows += node[i].len;
-    CK(launch_fill(acc_l, node_rows * BH, -INFINITY, st));
+    CK(launch_fill(acc_l, (sharded ? Lacc : node_rows) * BH, -INFINITY, st));
     ++launches;
 
     for (int64_t ti = gi; ti < ge; ++ti) {
@@ -337,7 +340,7 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
         while (s + 1 < node.size() &&
                !(segs[a].start >= node[s].start && segs[a].start < node[s].start + node[s].len))
           ++s;
-        dst[a] = node_off[s] + (segs[a].start - node[s].start);
+        dst[a] = sharded ? p->acc_row(segs[a].start) : node_off[s] + (segs[a].start - node[s].start);
       }
       const int b = int(run % S);
       if (buf_used[b]) CK(cudaStreamWaitEvent(sc.cs, ev_free[b], 0));
@@ -389,7 +392,7 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       // The last task has nothing after it to overlap the output download with, so it runs query
       // segment by query segment and each segment's final rows are downloaded while the next
       // segment computes (device-tier accumulator only).
-      const bool split_last = j == 0 && !split_first && ti == nmy - 1 &&
+      const bool split_last = j == 0 && !sharded && !split_first && ti == nmy - 1 &&
                               [&] { int n = 0; for (int a = 0; a < T.nseg; ++a) n += T.kept[a] != 0; return n; }() > 1;
       if (!split_first) {
         CK(cudaEventRecord(ev_ready[b], sc.cs));
@@ -400,7 +403,7 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
         }
       }
       std::vector<std::pair<int64_t, int64_t>> rest;   // final rows of this task still to emit
-      if (j == 0) rest = fin[size_t(ti)];
+      if (j == 0 && !sharded) rest = fin[size_t(ti)];
       if (split_last)
         for (int a = 0; a < T.nseg; ++a) {
           if (!T.kept[a]) continue;
@@ -527,7 +530,7 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
     stats->tasks_run = run;
     stats->tasks_skipped = int64_t(p->tasks.size()) - run;
     stats->kernel_launches = launches;
-    stats->peak_dev_bytes = p->predicted_peak;
+    stats->predicted_peak_bytes = p->predicted_peak;
   }
   (void)out_strides;
   return CQS_OK;

@@ -18,12 +18,32 @@ def test_header_symbols_exported():
     L = ctypes.CDLL(cqs.LIB_PATH)
     for name in declared:
         assert hasattr(L, name), name
-    assert cqs.lib().cqs_abi_version() == 3
+    assert cqs.lib().cqs_abi_version() == 4
 
 
-def test_struct_sizes_match_c_layout():
-    assert ctypes.sizeof(cqs.PlanDesc) == 104
-    assert ctypes.sizeof(cqs.PlanInfo) == 96
+def test_struct_sizes_match_c_layout(tmp_path):
+    """Size and every field offset of the ctypes mirrors equal the C compiler's for include/cqs.h."""
+    import os
+    import subprocess
+    structs = {"cqs_plan_desc": cqs.PlanDesc, "cqs_plan_info_t": cqs.PlanInfo,
+               "cqs_task_t": cqs.Task, "cqs_stats": cqs.Stats}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "cqs.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append('printf("%s %%zu\\n", sizeof(%s));' % (cname, cname))
+        for f in py._fields_:
+            lines.append('printf("%s.%s %%zu\\n", offsetof(%s, %s));' % (cname, f[0], cname, f[0]))
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(exe)], check=True)
+    got = dict(ln.split() for ln in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                     check=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(py), cname
+        for f in py._fields_:
+            assert int(got[cname + "." + f[0]]) == getattr(py, f[0]).offset, (cname, f[0])
 
 
 def test_invalid_interest_set_rejected():
@@ -57,3 +77,14 @@ def test_budget_infeasible():
     with pytest.raises(cqs.CqsError) as e:
         cqs.cqs_plan(N=131072, B=1, H=32, D=128, depth=-1, budget_bytes=1 << 30)
     assert e.value.status == cqs.CQS_E_INFEASIBLE
+
+
+def test_exec_order_must_be_a_permutation():
+    with pytest.raises(cqs.CqsError) as e:
+        cqs.cqs_plan(N=500, B=1, H=1, D=128, depth=1, exec_order=[0, 1, 2, 3, 4, 5, 5])
+    assert e.value.status == cqs.CQS_E_INVALID
+    with pytest.raises(cqs.CqsError) as e:
+        cqs.cqs_plan(N=500, B=1, H=1, D=128, depth=1, exec_order=[0, 1, 2])
+    assert e.value.status == cqs.CQS_E_INVALID
+    p = cqs.cqs_plan(N=500, B=1, H=1, D=128, depth=1, exec_order=[6, 5, 4, 3, 2, 1, 0])
+    assert p.info().my_tasks == 7

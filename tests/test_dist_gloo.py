@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, N, H, D, depth, outdir):
+def _worker(rank, world, port, N, H, D, depth, outdir, shard="lpt", qkv_loc="device"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import cqs_synth
@@ -34,11 +34,17 @@ def _worker(rank, world, port, N, H, D, depth, outdir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     q, k, v = (cqs_synth.numpy_tensor((1, H, N, D), 77, n) for n in ("q", "k", "v"))
-    plan = cqs.cqs_plan(N=N, B=1, H=H, D=D, depth=depth, in_dtype="f32", world=world, rank=rank)
+    plan = cqs.cqs_plan(N=N, B=1, H=H, D=D, depth=depth, in_dtype="f32", world=world, rank=rank,
+                        shard=shard, qkv_loc=qkv_loc, out_loc="host" if qkv_loc == "host" else None)
     info = plan.info()
-    # this rank's partial accumulator [N][H][D] + [N][H] (lse = -inf: nothing yet)
-    acc_o = np.zeros((N, H, D))
-    acc_l = np.full((N, H), -np.inf)
+    # this rank's rank-local accumulator: the rows cqs_partial_runs says it holds, in local order
+    runs = cqs.cqs_partial_runs(plan, rank, 0, N)
+    local_of = np.full(N, -1)
+    for g0, n, l0 in runs:
+        local_of[g0:g0 + n] = np.arange(l0, l0 + n)
+    assert info.acc_rows >= (local_of.max() + 1) and info.acc_rows % cqs.CQS_ACC_BLOCK_ROWS == 0
+    acc_o = np.zeros((info.acc_rows, H, D))
+    acc_l = np.full((info.acc_rows, H), -np.inf)
     mine = 0
     for t in range(info.n_tasks):
         task = plan.task(t)
@@ -47,27 +53,47 @@ def _worker(rank, world, port, N, H, D, depth, outdir):
         mine += 1
         e = O.build_subseq_entry(N, 7, I, tuple(task.quorum[i] for i in range(depth)))
         Oi, li = O.task_partial(q, k, v, e)
-        idx = e.token_ids
+        rows_kept = np.isfinite(li[0, 0])          # query rows with a kept key
+        idx = local_of[e.token_ids[rows_kept]]
+        assert (idx >= 0).all(), "a task's query row is not in its rank's accumulator"
         mo, ml = O.lse_merge([(acc_o[idx], acc_l[idx]),
-                              (Oi[0].transpose(1, 0, 2), li[0].transpose(1, 0))])
+                              (Oi[0].transpose(1, 0, 2)[rows_kept], li[0].transpose(1, 0)[rows_kept])])
         acc_o[idx], acc_l[idx] = mo, ml
     assert mine == info.my_tasks
-    ro, rl, row0, rows = cdist.exchange_partials(
-        torch.from_numpy(acc_o.reshape(N, H * D)), torch.from_numpy(acc_l), N, world, rank)
-    po, pl = cdist.split_parts(ro, rl, world, rows)
-    Om, lm = O.lse_merge([(p.numpy().reshape(rows, H, D), l_.numpy()) for p, l_ in zip(po, pl)])
+    ro, rl, part_off, part_row0 = cdist.exchange_partials(
+        plan, torch.from_numpy(acc_o.reshape(-1, H * D)), torch.from_numpy(acc_l))
+    row0, rows = cqs.cqs_shard_rows(N, world, rank)
+    # owner side (the GPU's cqs_exchange_merge, here with the oracle merge): per global row of the
+    # shard, the partials of every rank holding it
+    parts = [[] for _ in range(rows)]
+    for r in range(world):
+        for g0, n, l0 in cqs.cqs_partial_runs(plan, r, row0, rows):
+            for i in range(n):
+                x = part_off[r] + (l0 + i - part_row0[r])
+                parts[g0 + i - row0].append((ro[x].numpy().reshape(H, D), rl[x].numpy()))
+    Om = np.zeros((rows, H, D))
+    lm = np.zeros((rows, H))
+    for i, ps in enumerate(parts):
+        assert ps, "row %d held by no rank" % (row0 + i)
+        Om[i], lm[i] = O.lse_merge(ps)
     np.save(os.path.join(outdir, "o%d.npy" % rank), Om)
     np.save(os.path.join(outdir, "l%d.npy" % rank), lm)
-    np.save(os.path.join(outdir, "w%d.npy" % rank), np.array([info.my_work_pairs, row0, rows]))
+    np.save(os.path.join(outdir, "w%d.npy" % rank),
+            np.array([info.my_work_pairs, row0, rows, info.acc_rows]))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("N,depth", [(343, 3), (448, 1), (1030, 2)])
-def test_two_rank_exchange_reproduces_dense(N, depth, tmp_path):
+@pytest.mark.parametrize("shard,qkv_loc", [("lpt", "device"), ("contiguous", "device"),
+                                           ("contiguous", "host")])
+@pytest.mark.parametrize("N,depth", [(343, 3), (448, 1), (1030, 2), (2500, 3)])
+def test_two_rank_exchange_reproduces_dense(N, depth, shard, qkv_loc, tmp_path):
+    """Rank-local accumulators (held blocks only) + one all-to-all exchange over gloo: each owner's
+    shard equals dense attention; resident and streamed plans, LPT and contiguous sharding."""
     import cqs_synth
     from oracle import cqs_oracle as O
     world, H, D = 2, 2, 32
-    mp.start_processes(_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path)),
+    mp.start_processes(_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path), shard,
+                                      qkv_loc),
                        nprocs=world, start_method="fork")
     q, k, v = (cqs_synth.numpy_tensor((1, H, N, D), 77, n) for n in ("q", "k", "v"))
     Od, ld = O.dense_attention(q, k, v)
@@ -75,7 +101,7 @@ def test_two_rank_exchange_reproduces_dense(N, depth, tmp_path):
     ld = ld[0].transpose(1, 0)
     tot_work = 0
     for r in range(world):
-        w, row0, rows = np.load(tmp_path / ("w%d.npy" % r))
+        w, row0, rows, acc_rows = np.load(tmp_path / ("w%d.npy" % r))
         tot_work += w
         Om = np.load(tmp_path / ("o%d.npy" % r))
         lm = np.load(tmp_path / ("l%d.npy" % r))

@@ -151,6 +151,6 @@ def test_streamed_backward_budget_one_staging_buffer():
                                                        budget_bytes=budget,
                                                        grad_dtype=torch.float32)
     peak = torch.cuda.max_memory_allocated() - base
-    assert info["workspace_bytes"] <= budget < two and peak <= budget + 512
+    assert info["workspace_bytes"] <= budget < two and peak <= budget
     for a, b in zip((dq, dk, dv), res):
         assert (a.cuda() - b).abs().max().item() <= 1e-6 * max(1.0, b.abs().max().item())

@@ -23,7 +23,8 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo", schedule="uniform"):
+def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo", schedule="uniform",
+            shard="lpt", qkv_loc="device"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import cqs_synth
@@ -34,51 +35,86 @@ def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo", schedule="un
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     q, k, v = cqs_synth.torch_qkv(1, H, N, D, 4242, dtype=torch.bfloat16, device="cuda")
+    streamed = qkv_loc == "host"
+    if streamed:   # each rank stages only its tasks' segments from pinned host memory
+        q, k, v = (t.cpu().pin_memory() for t in (q, k, v))
     plan = cqs.cqs_plan(N=N, B=1, H=H, D=D, depth=depth, in_dtype="bf16", world=world, rank=rank,
-                        schedule=schedule)
-    dev_bytes, _ = cqs.cqs_forward_workspace_size(plan)
+                        schedule=schedule, shard=shard, qkv_loc=qkv_loc,
+                        out_loc="host" if streamed else "device")
+    info = plan.info()
+    dev_bytes, host_bytes = cqs.cqs_forward_workspace_size(plan)
+    assert host_bytes == 0
     ws = torch.empty(dev_bytes, dtype=torch.uint8, device="cuda")
-    out = torch.zeros(1, H, N, D, dtype=torch.bfloat16, device="cuda")
-    lse = torch.zeros(1, H, N, dtype=torch.float32, device="cuda")
-    cqs.cqs_attention_forward(plan, q, k, v, out, None, 0.0, 0, ws, None)
-    ao, al = cqs.cqs_partial_view(plan, ws)
-    base = ws.data_ptr()
-    acc_o = ws[ao - base: ao - base + N * H * D * 4].view(torch.float32).view(N, H * D)
-    acc_l = ws[al - base: al - base + N * H * 4].view(torch.float32).view(N, H)
+    row0, rows = cqs.cqs_shard_rows(N, world, rank)
+    assert info.shard_rows == rows
+    out = torch.zeros(1, H, rows, D, dtype=torch.bfloat16, device="cuda")   # owned shard only
+    lse = torch.zeros(1, H, rows, dtype=torch.float32, device="cuda")
+    cqs.cqs_attention_forward(plan, q, k, v, None, None, 0.0, 0, ws, None)
     torch.cuda.synchronize()
-    if mode == "p2p":   # exchange + merge in one kernel over peer (IPC-mapped) memory
-        px = cdist.PeerExchange(plan, ws, N, 1, H, D, world, rank)
-        row0, rows = px.row0, px.rows
+    if mode == "p2p":   # exchange + merge over peer (IPC-mapped) memory
+        px = cdist.PeerExchange(plan, ws)
         px.merge(out, lse)
         px.close()
-    else:
-        ro, rl, row0, rows = cdist.exchange_partials(acc_o.cpu(), acc_l.cpu(), N, world, rank)
-        cdist.merge_shard_gpu(ro.cuda(), rl.cuda(), world, rows, 1, H, D, out, lse, row0, N)
+    else:               # all-to-all (gloo: CPU copies) + cqs_exchange_merge on the GPU
+        acc_o, acc_l = cdist.partial_accumulator(plan, ws)
+        ro, rl, off, pr0 = cdist.exchange_partials(plan, acc_o.cpu(), acc_l.cpu())
+        cdist.merge_received(plan, ro.cuda(), rl.cuda(), off, pr0, out, lse)
     torch.cuda.synchronize()
-    np.save(os.path.join(outdir, "o%d.npy" % rank), out[0, :, row0:row0 + rows].float().cpu().numpy())
-    np.save(os.path.join(outdir, "l%d.npy" % rank), lse[0, :, row0:row0 + rows].cpu().numpy())
-    np.save(os.path.join(outdir, "s%d.npy" % rank), np.array([row0, rows]))
+    np.save(os.path.join(outdir, "o%d.npy" % rank), out[0].float().cpu().numpy())
+    np.save(os.path.join(outdir, "l%d.npy" % rank), lse[0].cpu().numpy())
+    np.save(os.path.join(outdir, "s%d.npy" % rank), np.array([row0, rows, info.acc_rows]))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode,schedule", [("gloo", "uniform"), ("p2p", "uniform"),
-                                           ("p2p", "hybrid")])
-@pytest.mark.parametrize("N,depth", [(3000, 2), (2401, 3), (5000, 1)])
-def test_two_ranks_one_gpu(N, depth, mode, schedule, tmp_path):
+def _check_shards(tmp_path, world, N, H, D, seed=4242):
     import cqs_synth
     from oracle import cqs_oracle as O
-    world, H, D = 2, 2, 128
-    mp.start_processes(_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path), mode,
-                                      schedule),
-                       nprocs=world, start_method="spawn")
-    q, k, v = cqs_synth.torch_qkv(1, H, N, D, 4242, dtype=torch.bfloat16)
-    Od, ld = O.dense_attention(*(t.double().numpy() for t in (q, k, v)))
+    q, k, v = cqs_synth.torch_qkv(1, H, N, D, seed, dtype=torch.bfloat16)
+    if N <= 6000:
+        Od, ld = O.dense_attention(*(t.double().numpy() for t in (q, k, v)))
+    rng = np.random.default_rng(N)
     for r in range(world):
-        row0, rows = np.load(tmp_path / ("s%d.npy" % r))
+        row0, rows, _ = np.load(tmp_path / ("s%d.npy" % r))
         o = np.load(tmp_path / ("o%d.npy" % r))
         l_ = np.load(tmp_path / ("l%d.npy" % r))
-        assert np.abs(o - Od[0, :, row0:row0 + rows]).max() <= 2e-2
-        assert np.abs(l_ - ld[0, :, row0:row0 + rows]).max() <= 1e-3
+        if N <= 6000:
+            assert np.abs(o - Od[0, :, row0:row0 + rows]).max() <= 2e-2
+            assert np.abs(l_ - ld[0, :, row0:row0 + rows]).max() <= 1e-3
+            continue
+        # sampled rows: both shard edges plus random rows, every head
+        sel = np.unique(np.concatenate([[0, rows - 1], rng.choice(rows, 150, replace=False)]))
+        for h in range(H):
+            Oref, lref = O.dense_attention_rows(*(t[0, h].double().numpy() for t in (q, k, v)),
+                                                row0 + sel)
+            assert np.abs(o[h, sel] - Oref).max() <= 2e-2
+            assert np.abs(l_[h, sel] - lref).max() <= 1e-3
+
+
+@pytest.mark.parametrize("mode,schedule,shard", [("gloo", "uniform", "lpt"),
+                                                 ("p2p", "uniform", "lpt"),
+                                                 ("p2p", "hybrid", "lpt"),
+                                                 ("p2p", "uniform", "contiguous"),
+                                                 ("gloo", "uniform", "contiguous")])
+@pytest.mark.parametrize("N,depth", [(3000, 2), (2401, 3), (5000, 1)])
+def test_two_ranks_one_gpu(N, depth, mode, schedule, shard, tmp_path):
+    world, H, D = 2, 2, 128
+    mp.start_processes(_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path), mode,
+                                      schedule, shard),
+                       nprocs=world, start_method="spawn")
+    _check_shards(tmp_path, world, N, H, D)
+
+
+@pytest.mark.parametrize("mode", ["p2p", "gloo"])
+@pytest.mark.parametrize("N,depth,D", [(20000, 3, 128), (12000, 4, 64)])
+def test_two_ranks_streamed_c4_shape(N, depth, D, mode, tmp_path):
+    """C4's multi-rank layout at small N: Q/K/V in pinned host memory, every rank stages only its
+    (contiguous) tasks' segments, keeps a rank-local accumulator, and one exchange finalizes the
+    owned shards."""
+    world, H = 2, 2
+    mp.start_processes(_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path), mode,
+                                      "uniform", "contiguous", "host"),
+                       nprocs=world, start_method="spawn")
+    _check_shards(tmp_path, world, N, H, D)
 
 
 def _bwd_worker(rank, world, port, N, H, D, depth, outdir, mode, schedule="uniform"):

@@ -54,8 +54,8 @@ def test_streamed_bf16_budget_tiers(N, H, D):
         out, lse, info, st, peak = run_streamed(q, k, v, budget, depth=kk)
         assert (info.depth, info.acc_depth, info.n_stage_buffers) == (kk, j, nb)
         budget = budget or info.predicted_peak_bytes
-        # peak is measured through torch's allocator, which rounds blocks up to 512 bytes
-        assert info.predicted_peak_bytes <= budget and peak <= budget + 512
+        # peak through torch's allocator: the model counts every tensor at its 512-byte granularity
+        assert info.predicted_peak_bytes <= budget and peak <= budget
         assert st.bytes_h2d > 0 and st.tasks_run == info.my_tasks
         check(out, lse, q, k, v, 2e-2, 1e-3)
 
@@ -80,7 +80,7 @@ def test_c3_streamed_16gib_sampled():
                .cpu().pin_memory() for nm in ("q", "k", "v"))
     torch.cuda.empty_cache()
     out, lse, info, st, peak = run_streamed(q, k, v, budget)
-    assert info.depth == 2 and peak <= budget + 512
+    assert info.depth == 2 and peak <= budget
     rng = np.random.default_rng(2)
     # 4 heads x 64 rows: random rows plus the first / last token and both sides of every level-1
     # and level-2 chunk boundary (BalancedChunkLayout, R1)
@@ -104,7 +104,7 @@ def test_streamed_batch2_f32_out():
     d = cqs.make_desc(N=1500, B=2, H=2, D=128, depth=-1, in_dtype="bf16", qkv_loc="host")
     budget, _ = cqs.cqs_memory_model(d, 2, 1, 1)
     out, lse, info, st, peak = run_streamed(q, k, v, budget, depth=2, out_dtype="f32")
-    assert info.depth == 2 and peak <= budget + 512
+    assert info.depth == 2 and peak <= budget
     check(out, lse, q, k, v, 2e-2, 1e-3)
 
 
@@ -188,5 +188,5 @@ def test_streamed_device_tier_first_last_split(N, depth, nb, D):
     budget = cqs.cqs_memory_model(d, depth, 0, nb)[0]
     out, lse, info, st, peak = run_streamed(q, k, v, budget, depth=depth)
     assert (info.depth, info.acc_depth, info.n_stage_buffers) == (depth, 0, nb)
-    assert peak <= budget + 512
+    assert peak <= budget
     check(out, lse, q, k, v, 2e-2, 1e-3)
