@@ -85,12 +85,18 @@ typedef struct {
                                 fewer rows — its accumulator (which holds only the rows its tasks
                                 touch, see cqs_partial_runs) shrinks, e.g. to <= 70% of N at
                                 C4 / world 8.  Ignored when world = 1.                          */
-  int32_t reserved0;         /* must be 0                                                       */
+  int32_t flags;             /* CQS_PLAN_SUBSET: exec_order lists a SUBSET of the tasks (distinct
+                                indices) and the call runs only those (of this rank), in that
+                                order — the output then holds the LSE merge of their partials
+                                only (rows they never touch: O = 0, lse = -inf).  For splitting
+                                one tree over several calls / schedulers and for sampled
+                                measurement (SURVEY §8d C5 protocol).  Other bits must be 0.   */
   const int64_t* exec_order; /* NULL, or a permutation of [0, n_tasks) (host memory, copied): the
                                 rank runs its tasks in this relative order instead of the
                                 lexicographic one.  Any order is exact (the LSE merge is
                                 associative and commutative, Eq. 3) up to fp rounding.
-                                CQS_E_INVALID if not a permutation of the planned task count.   */
+                                CQS_E_INVALID if not a permutation of the planned task count
+                                (without CQS_PLAN_SUBSET) or not distinct valid indices.        */
   int64_t n_exec_order;
 } cqs_plan_desc;
 
@@ -98,6 +104,7 @@ typedef struct {
 #define CQS_SCHED_HYBRID 1
 #define CQS_SHARD_LPT 0
 #define CQS_SHARD_CONTIGUOUS 1
+#define CQS_PLAN_SUBSET 1
 /* Rank-local accumulators (world > 1) are kept in blocks of this many consecutive rows. */
 #define CQS_ACC_BLOCK_ROWS 256
 

@@ -25,8 +25,12 @@ def _a256(x):
     return (x + 255) // 256 * 256
 
 
-def _a512(x):
-    return (x + 511) // 512 * 512
+def _alloc(x):
+    """Bytes a separately allocated device tensor occupies (R14): < 1 MiB -> 512-byte multiple
+    (shared small segment); otherwise its own segment of 2 MiB device pages."""
+    if x < (1 << 20):
+        return (x + 511) // 512 * 512
+    return (x + (2 << 20) - 1) // (2 << 20) * (2 << 20)
 
 
 def leaf_staged_rows(N, c, I, k):
@@ -66,12 +70,12 @@ def workspace_bytes(N, BH, D, e_in, streamed, out_host, staged_rows, acc_rows, n
 
 
 def device_bytes(N, B, H, D, e_in, e_out, streamed, out_host, staged_rows, acc_rows, nbuf):
-    """Each tensor at the caching allocator's 512-byte granularity (R14)."""
+    """Each tensor as the caller's allocator holds it (_alloc, R14)."""
     BH = B * H
-    caller = 0 if streamed else 3 * _a512(BH * N * D * e_in)
+    caller = 0 if streamed else 3 * _alloc(BH * N * D * e_in)
     if not out_host:
-        caller += _a512(BH * N * D * e_out) + _a512(4 * BH * N)
-    return caller + _a512(workspace_bytes(N, BH, D, e_in, streamed, out_host, staged_rows,
+        caller += _alloc(BH * N * D * e_out) + _alloc(4 * BH * N)
+    return caller + _alloc(workspace_bytes(N, BH, D, e_in, streamed, out_host, staged_rows,
                                           acc_rows, nbuf))
 
 
@@ -114,4 +118,4 @@ def backward_workspace_bytes(N, BH, D, streamed=False, staged_rows=0, nbuf=0):
         b += nbuf * 4 * _a256(BH * staged_rows * D * 2)
         F = min(max((64 << 20) // (BH * D * 4), 256), 65536, N)
         b += 2 * (_a256(F * BH * D * 4) + _a256(F * BH * 4))
-    return _a512(b)
+    return _alloc(b)

@@ -26,6 +26,7 @@ CQS_LOC_DEVICE, CQS_LOC_PINNED_HOST = 0, 1
 CQS_SCHED_UNIFORM, CQS_SCHED_HYBRID = 0, 1
 CQS_SHARD_LPT, CQS_SHARD_CONTIGUOUS = 0, 1
 CQS_ACC_BLOCK_ROWS = 256
+CQS_PLAN_SUBSET = 1
 CQS_MAX_DEPTH, CQS_MAX_SEGS = 12, 32
 STATUS_NAMES = {0: "CQS_OK", 1: "CQS_E_VERIFY", 2: "CQS_E_INFEASIBLE", 3: "CQS_E_INVALID",
                 4: "CQS_E_CUDA", 5: "CQS_E_NCCL", 6: "CQS_E_OOM", 7: "CQS_E_UNSUPPORTED"}
@@ -54,7 +55,7 @@ class PlanDesc(C.Structure):
                 ("world", C.c_int32), ("rank", C.c_int32), ("schedule", C.c_int32),
                 ("n_level_sets", C.c_int32), ("level_c", C.POINTER(C.c_int32)),
                 ("level_offsets", C.POINTER(C.c_int32)), ("shard", C.c_int32),
-                ("reserved0", C.c_int32), ("exec_order", C.POINTER(C.c_int64)),
+                ("flags", C.c_int32), ("exec_order", C.POINTER(C.c_int64)),
                 ("n_exec_order", C.c_int64)]
 
 
@@ -161,10 +162,11 @@ def _loc_code(x):
 
 def make_desc(N, B, H, D, depth=1, budget_bytes=0, in_dtype="bf16", out_dtype=None,
               qkv_loc="device", out_loc=None, world=1, rank=0, c=7, offsets=(0, 1, 3),
-              schedule="uniform", levels=None, shard="lpt", exec_order=None):
+              schedule="uniform", levels=None, shard="lpt", exec_order=None, subset=False):
     """levels: optional [(c_t, offsets_t), ...] interest sets for divide levels 0, 1, ...
     (deeper levels use (c, offsets)).  shard: "lpt" | "contiguous" (world > 1 assignment).
-    exec_order: optional permutation of the task indices (this rank's execution order)."""
+    exec_order: optional permutation of the task indices (this rank's execution order); with
+    subset=True a list of distinct task indices: only those run (CQS_PLAN_SUBSET)."""
     offs = (C.c_int32 * len(offsets))(*offsets)
     levels = list(levels or [])
     lc = (C.c_int32 * max(len(levels), 1))(*[int(c_t) for c_t, _ in levels])
@@ -180,7 +182,7 @@ def make_desc(N, B, H, D, depth=1, budget_bytes=0, in_dtype="bf16", out_dtype=No
                      schedule, schedule),
                  n_level_sets=len(levels), level_c=lc, level_offsets=lo,
                  shard={"lpt": CQS_SHARD_LPT, "contiguous": CQS_SHARD_CONTIGUOUS}.get(shard, shard),
-                 reserved0=0)
+                 flags=CQS_PLAN_SUBSET if subset else 0)
     eo = None
     if exec_order is not None:
         eo = (C.c_int64 * max(len(exec_order), 1))(*[int(x) for x in exec_order])

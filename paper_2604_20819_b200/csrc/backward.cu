@@ -68,7 +68,7 @@ static BwdLayout bwd_layout(const cqs_plan_t* p, int nbuf) {
     L.chunk_bytes = L.chunk_lse + align256(uint64_t(L.F) * BH * 4);
     L.total = L.chunk + 2 * L.chunk_bytes;
   }
-  L.total = align512(L.total);   // the caller's allocator granularity (R14)
+  L.total = alloc_bytes(L.total);   // the caller's allocator granularity (R14)
   return L;
 }
 

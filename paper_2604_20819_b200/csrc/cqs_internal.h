@@ -87,7 +87,7 @@ MemModel memory_model(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_r
 void held_blocks(const std::vector<Task>& tasks, const std::vector<Seg>& segs, int64_t N,
                  int32_t r, std::vector<uint8_t>& held);
 uint64_t align256(uint64_t x);
-uint64_t align512(uint64_t x);
+uint64_t alloc_bytes(uint64_t x);
 // Section offsets of the device workspace (forward.cu must follow memory_model exactly).
 struct WsLayout {
   uint64_t acc_o, acc_lse, stage, stage_bytes_per_buf, flush, total;

@@ -28,7 +28,14 @@ cqs_status fail(cqs_status st, const std::string& msg) {
 }
 
 uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
-uint64_t align512(uint64_t x) { return (x + 511) & ~uint64_t(511); }
+// Bytes a device tensor of x bytes occupies in the caller's caching allocator (R14): below 1 MiB a
+// 512-byte multiple carved from a shared small segment; from 1 MiB up its own segment of 2 MiB
+// device pages (the driver's allocation granularity), so the allocator's view never exceeds it and
+// a separately allocated tensor costs exactly this much free device memory.
+uint64_t alloc_bytes(uint64_t x) {
+  if (x < (uint64_t(1) << 20)) return (x + 511) & ~uint64_t(511);
+  return (x + (uint64_t(2) << 20) - 1) & ~((uint64_t(2) << 20) - 1);
+}
 
 static int64_t elem_size(cqs_dtype t) { return t == CQS_BF16 ? 2 : 4; }
 
@@ -63,14 +70,13 @@ MemModel memory_model(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_r
                       int32_t n_stage_buffers, int64_t out_rows) {
   const uint64_t BH = uint64_t(d.B) * d.H, N = d.N, D = d.D, R = uint64_t(out_rows);
   MemModel m{};
-  // every tensor counted at the caching allocator's 512-byte granularity (R14): a caller that
-  // allocates Q, K, V, O, lse and the workspace as separate torch tensors sees exactly this many
-  // allocated bytes
+  // every tensor counted as the caller's allocator holds it (alloc_bytes, R14): Q, K, V, O, lse
+  // and the workspace allocated as separate tensors never occupy more than this
   m.caller_dev = 0;
-  if (d.qkv_loc == CQS_LOC_DEVICE) m.caller_dev += 3 * align512(BH * N * D * elem_size(d.in_dtype));
+  if (d.qkv_loc == CQS_LOC_DEVICE) m.caller_dev += 3 * alloc_bytes(BH * N * D * elem_size(d.in_dtype));
   if (d.out_loc == CQS_LOC_DEVICE || d.world > 1)
-    m.caller_dev += align512(BH * R * D * elem_size(d.out_dtype)) + align512(4 * BH * R);
-  m.dev_ws = align512(ws_layout(d, staged_rows, acc_rows, n_stage_buffers).total);
+    m.caller_dev += alloc_bytes(BH * R * D * elem_size(d.out_dtype)) + alloc_bytes(4 * BH * R);
+  m.dev_ws = alloc_bytes(ws_layout(d, staged_rows, acc_rows, n_stage_buffers).total);
   // pinned host accumulator of the host tier (world = 1 streamed plans with j > 0)
   m.host_ws = (d.world == 1 && acc_rows < d.N) ? align256(N * BH * D * 4) + align256(N * BH * 4) : 0;
   return m;
@@ -468,7 +474,9 @@ static cqs_status validate_desc(const cqs_plan_desc* d, Levels& lv) {
     return fail(CQS_E_INVALID, "schedule must be CQS_SCHED_UNIFORM or CQS_SCHED_HYBRID");
   if (d->shard != CQS_SHARD_LPT && d->shard != CQS_SHARD_CONTIGUOUS)
     return fail(CQS_E_INVALID, "shard must be CQS_SHARD_LPT or CQS_SHARD_CONTIGUOUS");
-  if (d->reserved0 != 0) return fail(CQS_E_INVALID, "reserved0 must be 0");
+  if (d->flags & ~CQS_PLAN_SUBSET) return fail(CQS_E_INVALID, "unknown flags");
+  if ((d->flags & CQS_PLAN_SUBSET) && !d->exec_order)
+    return fail(CQS_E_INVALID, "CQS_PLAN_SUBSET needs exec_order");
   if (d->n_exec_order < 0 || (d->n_exec_order > 0 && !d->exec_order))
     return fail(CQS_E_INVALID, "exec_order NULL with n_exec_order > 0");
   if (d->schedule == CQS_SCHED_HYBRID && d->qkv_loc == CQS_LOC_PINNED_HOST)
@@ -609,23 +617,37 @@ cqs_status cqs_plan(const cqs_plan_desc* desc, cqs_plan_t** out) {
       p->my_order.push_back(i);
       p->my_work += p->tasks[size_t(i)].work;
     }
-  if (d.exec_order) {   // caller's execution order (any order is exact, Eq. 3)
+  if (d.exec_order) {   // caller's execution order (any order is exact, Eq. 3) or subset
     const int64_t n = int64_t(p->tasks.size());
-    if (d.n_exec_order != n) {
+    const bool subset = d.flags & CQS_PLAN_SUBSET;
+    if (!subset && d.n_exec_order != n) {
       delete p;
       return fail(CQS_E_INVALID, "exec_order must list all " + std::to_string(n) + " tasks");
     }
     std::vector<int64_t> pos(size_t(n), -1);
-    for (int64_t i = 0; i < n; ++i) {
+    for (int64_t i = 0; i < d.n_exec_order; ++i) {
       const int64_t t = d.exec_order[i];
       if (t < 0 || t >= n || pos[size_t(t)] >= 0) {
         delete p;
-        return fail(CQS_E_INVALID, "exec_order is not a permutation of the task indices");
+        return fail(CQS_E_INVALID, "exec_order entries must be distinct task indices");
       }
       pos[size_t(t)] = i;
     }
-    std::stable_sort(p->my_order.begin(), p->my_order.end(),
-                     [&](int64_t a, int64_t b) { return pos[size_t(a)] < pos[size_t(b)]; });
+    if (subset) {   // only the listed tasks of this rank, in the listed order
+      std::vector<int64_t> mine;
+      p->my_work = 0;
+      for (int64_t i = 0; i < d.n_exec_order; ++i) {
+        const Task& T = p->tasks[size_t(d.exec_order[i])];
+        if (T.rank == d.rank && T.work > 0) {
+          mine.push_back(d.exec_order[i]);
+          p->my_work += T.work;
+        }
+      }
+      p->my_order.swap(mine);
+    } else {
+      std::stable_sort(p->my_order.begin(), p->my_order.end(),
+                       [&](int64_t a, int64_t b) { return pos[size_t(a)] < pos[size_t(b)]; });
+    }
   }
   if (sharded) {
     // rank-local accumulator: held blocks packed in increasing global order

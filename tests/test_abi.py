@@ -88,3 +88,12 @@ def test_exec_order_must_be_a_permutation():
     assert e.value.status == cqs.CQS_E_INVALID
     p = cqs.cqs_plan(N=500, B=1, H=1, D=128, depth=1, exec_order=[6, 5, 4, 3, 2, 1, 0])
     assert p.info().my_tasks == 7
+
+
+def test_subset_plan_runs_only_listed_tasks():
+    p = cqs.cqs_plan(N=500, B=1, H=1, D=128, depth=2, exec_order=[40, 3, 17], subset=True)
+    assert p.info().my_tasks == 3 and p.info().n_tasks == 49
+    w = sum(p.task(t).work for t in (40, 3, 17))
+    assert p.info().my_work_pairs == w
+    with pytest.raises(cqs.CqsError):
+        cqs.cqs_plan(N=500, B=1, H=1, D=128, depth=2, exec_order=[40, 40], subset=True)

@@ -227,3 +227,41 @@ def test_bf16_tile_boundaries(N, depth, D):
     out, lse = cqs.attention(q, k, v, depth=depth)
     torch.cuda.synchronize()
     check_bf16(out, lse, *ref_dense(q, k, v))
+
+
+@pytest.mark.parametrize("streamed", [False, True])
+def test_subset_calls_merge_to_full_attention(streamed):
+    """CQS_PLAN_SUBSET: the tree split over two calls (even / odd task indices), each call's
+    (O, lse) the LSE merge of its tasks only; merging the two results with cqs_merge (Eq. 3,
+    P:48-52) gives full attention."""
+    B, H, N, D, depth = 1, 2, 2500, 128, 2
+    q, k, v = gen(B, H, N, D, 2024, bf16=True)
+    halves = [list(range(0, 49, 2)), list(range(1, 49, 2))]
+    res = []
+    for sub in halves:
+        kw = dict(N=N, B=B, H=H, D=D, depth=depth, exec_order=sub, subset=True)
+        if streamed:
+            p = cqs.cqs_plan(qkv_loc="host", out_loc="host", out_dtype="f32", **kw)
+            dv, hb = cqs.cqs_forward_workspace_size(p)
+            ws = torch.empty(dv, dtype=torch.uint8, device=DEV)
+            hws = torch.empty(max(hb, 256), dtype=torch.uint8).pin_memory() if hb else None
+            out = torch.empty(q.shape, dtype=torch.float32).pin_memory()
+            lse = torch.empty(q.shape[:3], dtype=torch.float32).pin_memory()
+            qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
+            cqs.cqs_attention_forward(p, qh, kh, vh, out, lse, 0.0, 0, ws, hws)
+        else:
+            p = cqs.cqs_plan(out_dtype="f32", **kw)
+            ws = torch.empty(cqs.cqs_forward_workspace_size(p)[0], dtype=torch.uint8, device=DEV)
+            out = torch.empty(q.shape, dtype=torch.float32, device=DEV)
+            lse = torch.empty(q.shape[:3], dtype=torch.float32, device=DEV)
+            cqs.cqs_attention_forward(p, q, k, v, out, lse, 0.0, 0, ws, None)
+        torch.cuda.synchronize()
+        assert p.info().my_tasks <= len(sub)
+        # token-major partial for cqs_merge: [N][B*H][D], [N][B*H]
+        res.append((out.to(DEV).permute(2, 0, 1, 3).reshape(N, B * H, D).contiguous(),
+                    lse.to(DEV).permute(2, 0, 1).reshape(N, B * H).contiguous()))
+    fo = torch.empty(B, H, N, D, dtype=torch.float32, device=DEV)
+    fl = torch.empty(B, H, N, dtype=torch.float32, device=DEV)
+    cqs.cqs_merge(N, B, H, D, [r[0] for r in res], [r[1] for r in res], out=fo, lse_out=fl)
+    torch.cuda.synchronize()
+    check_bf16(fo, fl, *ref_dense(q, k, v))
