@@ -88,7 +88,10 @@ typedef struct {
   int32_t flags;             /* CQS_PLAN_SUBSET: exec_order lists a SUBSET of the tasks (distinct
                                 indices) and the call runs only those (of this rank), in that
                                 order — the output then holds the LSE merge of their partials
-                                only (rows they never touch: O = 0, lse = -inf).  For splitting
+                                only (rows they never touch: O = 0 and lse = -inf, or left
+                                unwritten by the streamed executor with a host-tier
+                                accumulator, which never reads or writes host rows outside the
+                                listed tasks' subsequences).  For splitting
                                 one tree over several calls / schedulers and for sampled
                                 measurement (SURVEY §8d C5 protocol).  Other bits must be 0.   */
   const int64_t* exec_order; /* NULL, or a permutation of [0, n_tasks) (host memory, copied): the

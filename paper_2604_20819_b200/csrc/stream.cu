@@ -291,7 +291,9 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       }
       const int64_t next = e < ev.size() ? std::min<int64_t>(ev[e].first, N) : N;
       if (heap.empty()) {
-        direct_final = false;   // a row in no subtree (cannot happen at world 1): final pass
+        // a row in no subtree: only with CQS_PLAN_SUBSET (a full tree at world 1 covers every
+        // row); such rows are left unwritten — reading the host accumulator for them would touch
+        // all of it
       } else {
         auto& v = fin_g[size_t(heap.front() - 1)];
         if (!v.empty() && v.back().first + v.back().second == row)

@@ -245,8 +245,8 @@ def test_subset_calls_merge_to_full_attention(streamed):
             dv, hb = cqs.cqs_forward_workspace_size(p)
             ws = torch.empty(dv, dtype=torch.uint8, device=DEV)
             hws = torch.empty(max(hb, 256), dtype=torch.uint8).pin_memory() if hb else None
-            out = torch.empty(q.shape, dtype=torch.float32).pin_memory()
-            lse = torch.empty(q.shape[:3], dtype=torch.float32).pin_memory()
+            out = torch.zeros(q.shape, dtype=torch.float32).pin_memory()
+            lse = torch.full(q.shape[:3], -math.inf, dtype=torch.float32).pin_memory()
             qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
             cqs.cqs_attention_forward(p, qh, kh, vh, out, lse, 0.0, 0, ws, hws)
         else:
