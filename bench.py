@@ -624,7 +624,11 @@ def main():
     peaks, peak_src = load_peaks()
     kname = "attn_bf16_sm100_2cta_kernel" if D == 128 else "attn_bf16_sm100_kernel<%d>" % D
     traffic = ncu_traffic(kname)
-    peak = peaks.get("bf16_tflops", 1645.9)
+    # the peak that matches the timing (task rules): the attention kernels run back to back for the
+    # whole timed region (>= 1 s, under sw_power_cap), so the SUSTAINED measured bf16 peak; the
+    # burst figure is reported beside it
+    peak_burst = peaks.get("bf16_tflops", 1645.9)
+    peak = peaks.get("bf16_tflops_sustained", peak_burst)
     value = flops / (ms * 1e-3) / 1e12
     # attention-kernel-only rate: rank 0's algorithmic FLOPs / summed kernel durations (CUDA events)
     attn_tf = (flops * info.my_work_pairs / info.total_work_pairs) / (attn_ms / args.steps * 1e-3) / 1e12 \
@@ -651,14 +655,16 @@ def main():
                    "parallelism": "task-sharded x%d" % world,
                    "exchange": args.exchange if world > 1 else None},
         "tokens_per_s": N * B / (ms * 1e-3),
-        "pct_tensor_peak": value / (world * peak),
+        "pct_tensor_peak": value / (world * peak_burst),
         "roofline": {"bound": "tensor", "achieved": attn_tf, "peak": peak, "unit": "TFLOP/s",
                      "frac": (attn_tf / peak) if attn_tf else None,
                      "traffic": traffic[0] if traffic else None,
                      "traffic_source": traffic[1] if traffic else None,
-                     "kernel": kname, "peak_source": peak_src + " bf16_tflops (burst)",
-                     "frac_of_sustained": (attn_tf / peaks.get("bf16_tflops_sustained", peak))
-                     if attn_tf else None,
+                     "kernel": kname,
+                     "peak_source": peak_src + " bf16_tflops_sustained (cuBLAS 8192^3 back to "
+                                    "back for 4 s: the kernel is timed inside a long run)",
+                     "peak_burst": peak_burst,
+                     "frac_of_burst": (attn_tf / peak_burst) if attn_tf else None,
                      "flops_per_launch": flops * info.my_work_pairs / info.total_work_pairs
                      / max(1, info.my_tasks),
                      "launches_per_step": info.my_tasks,
@@ -675,6 +681,7 @@ def main():
         bwd["roofline"] = {"bound": "tensor", "achieved": bwd["kernel_tflops_executed"],
                            "peak": peak, "unit": "TFLOP/s",
                            "frac": bwd["kernel_tflops_executed"] / peak,
+                           "frac_of_burst": bwd["kernel_tflops_executed"] / peak_burst,
                            "kernels": "bwd_dkdv + bwd_dq", "peak_source": line["roofline"]["peak_source"]}
     print(json.dumps(line))
     if world > 1:
