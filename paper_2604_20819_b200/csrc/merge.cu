@@ -33,93 +33,99 @@ __device__ __forceinline__ void store4(__nv_bfloat16* dst, float4 v) {
   *reinterpret_cast<uint2*>(dst) = u;
 }
 
-// One warp per (row, plane) unit per step, kUnits units per warp iteration so that every lane has
-// kUnits x (parts + 1) independent 16-byte loads in flight; the LSE weights of a unit are computed
-// redundantly by the 32 lanes (per unit, not per element).
-constexpr int kUnits = 4;
 
+__device__ __forceinline__ float fast_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fast_lg2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Eq. 3 weights of one unit in base 2 (MUFU ex2 / lg2: the accurate expf / logf and the 64-bit
+// index divisions of the first version ran on the XU pipe and held the R = 8 merge at 70% of HBM
+// bandwidth).  NP = the parts this instantiation supports (a power of two >= parts.n).
+template <int NP>
 __device__ __forceinline__ void unit_weights(const MergeParts& parts, const float* acc_lse,
-                                             int64_t unit, float (&w)[kMaxMergeParts + 1],
-                                             float& lse) {
+                                             int64_t unit, float (&w)[NP + 1], float& lse) {
+  constexpr float kLog2e = 1.4426950408889634f, kLn2 = 0.69314718055994531f;
   const float la = acc_lse ? acc_lse[unit] : -INFINITY;
   float mx = la;
-  for (int j = 0; j < parts.n; ++j) mx = fmaxf(mx, parts.l[j][unit]);
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    w[j] = j < parts.n ? parts.l[j][unit] : -INFINITY;
+    mx = fmaxf(mx, w[j]);
+  }
   if (mx == -INFINITY) {
 #pragma unroll
-    for (int j = 0; j <= kMaxMergeParts; ++j) w[j] = 0.f;
+    for (int j = 0; j <= NP; ++j) w[j] = 0.f;
     lse = -INFINITY;
     return;
   }
-  float s = 0.f;
-  w[kMaxMergeParts] = la != -INFINITY ? expf(la - mx) : 0.f;
-  s += w[kMaxMergeParts];
+  const float mb = mx * kLog2e;
+  // exp(l - mx) = 2^(l log2e - mx log2e); -inf entries give 2^-inf = 0
+  w[NP] = fast_ex2(fmaf(la, kLog2e, -mb));
+  float s = w[NP];
 #pragma unroll
-  for (int j = 0; j < kMaxMergeParts; ++j) {
-    float x = 0.f;
-    if (j < parts.n) {
-      const float lj = parts.l[j][unit];
-      x = lj != -INFINITY ? expf(lj - mx) : 0.f;
-    }
-    w[j] = x;
-    s += x;
+  for (int j = 0; j < NP; ++j) {
+    w[j] = fast_ex2(fmaf(w[j], kLog2e, -mb));
+    s += w[j];
   }
   const float inv = 1.f / s;
 #pragma unroll
-  for (int j = 0; j <= kMaxMergeParts; ++j) w[j] *= inv;
-  lse = mx + logf(s);
+  for (int j = 0; j <= NP; ++j) w[j] *= inv;
+  lse = mx + fast_lg2(s) * kLn2;
 }
 
-template <typename OutT>
+// One unit = one (row, plane) of D fp32 values.  min(32, D/4) lanes share a unit (one float4
+// column each, looping when D/4 > 32), so a warp covers 32 / lanes units per iteration; every
+// lane issues its NP part loads back to back (NP x 16 B in flight per lane) and the weights are
+// recomputed by each lane of the unit from broadcast lse loads.
+template <typename OutT, int NP, typename Idx>
 __global__ void __launch_bounds__(256)
-    merge_kernel(int64_t rows, int BH, int H, int D, MergeParts parts, float* __restrict__ acc_o,
+    merge_kernel(Idx nunits, int BH, int H, int D4, MergeParts parts, float* __restrict__ acc_o,
                  float* __restrict__ acc_lse, bool acc_write, OutT* __restrict__ out, int64_t sB,
                  int64_t sH, int64_t sN, int64_t out_row0, int64_t n_total,
                  float* __restrict__ lse_out) {
   const int lane = threadIdx.x & 31;
-  const int64_t nunits = rows * BH;
-  const int64_t warp0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  const int D4 = D >> 2;
-  for (int64_t u0 = warp0 * kUnits; u0 < nunits; u0 += nwarps * kUnits) {
-    for (int d4 = lane; d4 < D4; d4 += 32) {
-      float4 v[kUnits];
-      float lse[kUnits];
+  const int lpu = D4 < 32 ? D4 : 32, upw = 32 / lpu;
+  const int lu = lane / lpu, sub = lane - lu * lpu;
+  if (lu >= upw) return;
+  const Idx warp0 = Idx((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5);
+  const Idx nwarps = Idx((int64_t(gridDim.x) * blockDim.x) >> 5);
+  for (Idx unit = warp0 * upw + lu; unit < nunits; unit += nwarps * upw) {
+    float w[NP + 1];
+    float lse;
+    unit_weights<NP>(parts, acc_lse, int64_t(unit), w, lse);
+    const Idx r = unit / Idx(BH);
+    const int p = int(unit - r * Idx(BH));
+    const int bb = p / H, hh = p - bb * H;
+    for (int d4 = sub; d4 < D4; d4 += lpu) {
+      const int64_t f = int64_t(unit) * D4 + d4;
+      float4 x[NP + 1];
 #pragma unroll
-      for (int u = 0; u < kUnits; ++u) {
-        const int64_t unit = u0 + u;
-        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (unit >= nunits) continue;
-        float w[kMaxMergeParts + 1];
-        unit_weights(parts, acc_lse, unit, w, lse[u]);
-        const int64_t f = unit * D4 + d4;
-        if (w[kMaxMergeParts] != 0.f) {
-          const float4 x = reinterpret_cast<const float4*>(acc_o)[f];
-          const float a = w[kMaxMergeParts];
-          v[u] = make_float4(a * x.x, a * x.y, a * x.z, a * x.w);
-        }
-        for (int j = 0; j < parts.n; ++j) {
-          if (w[j] == 0.f) continue;
-          const float4 x = reinterpret_cast<const float4*>(parts.o[j])[f];
-          v[u].x = fmaf(w[j], x.x, v[u].x);
-          v[u].y = fmaf(w[j], x.y, v[u].y);
-          v[u].z = fmaf(w[j], x.z, v[u].z);
-          v[u].w = fmaf(w[j], x.w, v[u].w);
-        }
-      }
+      for (int j = 0; j < NP; ++j)
+        if (w[j] != 0.f) x[j] = reinterpret_cast<const float4*>(parts.o[j])[f];
+      if (w[NP] != 0.f) x[NP] = reinterpret_cast<const float4*>(acc_o)[f];
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int u = 0; u < kUnits; ++u) {
-        const int64_t unit = u0 + u;
-        if (unit >= nunits) continue;
-        if (acc_write) reinterpret_cast<float4*>(acc_o)[unit * D4 + d4] = v[u];
-        const int64_t r = unit / BH;
-        const int p = int(unit - r * BH);
-        if (out)
-          store4(out + int64_t(p / H) * sB + int64_t(p % H) * sH + (out_row0 + r) * sN + 4 * d4, v[u]);
-        if (d4 == 0) {
-          if (acc_write) acc_lse[unit] = lse[u];
-          if (lse_out) lse_out[int64_t(p) * n_total + out_row0 + r] = lse[u];
-        }
+      for (int j = 0; j <= NP; ++j) {
+        if (w[j] == 0.f) continue;
+        v.x = fmaf(w[j], x[j].x, v.x);
+        v.y = fmaf(w[j], x[j].y, v.y);
+        v.z = fmaf(w[j], x[j].z, v.z);
+        v.w = fmaf(w[j], x[j].w, v.w);
       }
+      if (acc_write) reinterpret_cast<float4*>(acc_o)[f] = v;
+      if (out)
+        store4(out + int64_t(bb) * sB + int64_t(hh) * sH + (out_row0 + int64_t(r)) * sN + 4 * d4, v);
+    }
+    if (sub == 0) {
+      if (acc_write) acc_lse[unit] = lse;
+      if (lse_out) lse_out[int64_t(p) * n_total + out_row0 + int64_t(r)] = lse;
     }
   }
 }
@@ -205,15 +211,27 @@ cudaError_t launch_merge(int64_t rows, int B, int H, int D, int n_parts, const f
 #undef CQS_FIN
     return cudaGetLastError();
   }
-  const int64_t blocks = std::min<int64_t>((nunits + 8 * kUnits - 1) / (8 * kUnits), 148 * 32);
-  if (!bf)
-    merge_kernel<float><<<unsigned(blocks), 256, 0, st>>>(
-        rows, BH, H, D, mp, acc_o, acc_lse, acc_write, static_cast<float*>(out), sB, sH, sN,
-        out_row0, n_total, lse_out);
-  else
-    merge_kernel<__nv_bfloat16><<<unsigned(blocks), 256, 0, st>>>(
-        rows, BH, H, D, mp, acc_o, acc_lse, acc_write, static_cast<__nv_bfloat16*>(out), sB, sH,
-        sN, out_row0, n_total, lse_out);
+  const int D4 = D / 4, lpu = D4 < 32 ? D4 : 32, upw = 32 / lpu;
+  const int64_t warps = (nunits + upw - 1) / upw;
+  const int64_t blocks = std::min<int64_t>((warps + 7) / 8, 148 * 64);
+  const bool small = nunits + int64_t(blocks) * 256 < (int64_t(1) << 31);
+#define CQS_MERGE(T, NPV, I)                                                                   \
+  merge_kernel<T, NPV, I><<<unsigned(blocks), 256, 0, st>>>(                                   \
+      I(nunits), BH, H, D4, mp, acc_o, acc_lse, acc_write, static_cast<T*>(out), sB, sH, sN,   \
+      out_row0, n_total, lse_out)
+#define CQS_MERGE_NP(T, I)                          \
+  if (n_parts <= 1) CQS_MERGE(T, 1, I);             \
+  else if (n_parts <= 2) CQS_MERGE(T, 2, I);        \
+  else if (n_parts <= 4) CQS_MERGE(T, 4, I);        \
+  else if (n_parts <= 8) CQS_MERGE(T, 8, I);        \
+  else CQS_MERGE(T, 16, I);
+  if (bf) {
+    if (small) { CQS_MERGE_NP(__nv_bfloat16, uint32_t) } else { CQS_MERGE_NP(__nv_bfloat16, int64_t) }
+  } else {
+    if (small) { CQS_MERGE_NP(float, uint32_t) } else { CQS_MERGE_NP(float, int64_t) }
+  }
+#undef CQS_MERGE_NP
+#undef CQS_MERGE
   return cudaGetLastError();
 }
 

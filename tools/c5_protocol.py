@@ -53,7 +53,7 @@ def as_tensor(addr, shape, dtype):
     n = 1
     for s in shape:
         n *= s
-    esz = 2 if dtype == torch.bfloat16 else 4
+    esz = {torch.bfloat16: 2, torch.float32: 4, torch.uint8: 1}[dtype]
     raw = np.ctypeslib.as_array((ctypes.c_uint8 * (n * esz)).from_address(addr))
     t = torch.from_numpy(raw)
     return t.view(dtype).view(*shape)
