@@ -109,6 +109,38 @@ void build_task_params_ext(const cqs_plan_t* p, const Task& T, int rows_per_item
       tp);
 }
 
+// Descriptor of an explicit segment list (the streamed executor's first task split into pieces):
+// nseg segments of len[a] rows, kept[a] over those segments.
+void build_task_params_raw(int BH, int H, int nseg, const int64_t* len, const uint32_t* kept,
+                           int rows_per_item, const int64_t* src_rows, const int64_t* dst_rows,
+                           TaskParams& tp) {
+  std::memset(&tp, 0, sizeof(tp));
+  tp.nseg = nseg;
+  tp.BH = BH;
+  tp.H = H;
+  int64_t keywork[CQS_MAX_SEGS] = {};
+  int act[CQS_MAX_SEGS], na = 0;
+  for (int a = 0; a < nseg; ++a) {
+    tp.seg_src[a] = int32_t(src_rows[a]);
+    tp.seg_dst[a] = int32_t(dst_rows[a]);
+    tp.seg_len[a] = int32_t(len[a]);
+    tp.kept[a] = kept[a];
+    for (int b = 0; b < nseg; ++b)
+      if (kept[a] >> b & 1) keywork[a] += len[b];
+    if (kept[a]) act[na++] = a;
+  }
+  std::stable_sort(act, act + na, [&](int x, int y) { return keywork[x] > keywork[y]; });
+  int items = 0;
+  for (int i = 0; i < na; ++i) {
+    tp.order[i] = act[i];
+    items += int((tp.seg_len[act[i]] + rows_per_item - 1) / rows_per_item);
+    tp.item_end[i] = items;
+  }
+  for (int i = na; i < CQS_MAX_SEGS; ++i) tp.item_end[i] = items + 1;
+  tp.n_active = na;
+  tp.n_items = items;
+}
+
 cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, const void* v,
                             void* out, const int64_t* out_strides, float* lse, float scale,
                             uint8_t* ws, uint8_t* host_ws, cudaStream_t st, cqs_stats* stats);

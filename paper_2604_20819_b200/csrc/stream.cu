@@ -41,6 +41,9 @@ int attn_rows_per_item(int D);
 int attn_box_rows(int D, int which);
 void build_task_params_ext(const cqs_plan_t* p, const Task& T, int rows_per_item,
                            const int64_t* src_rows, const int64_t* dst_rows, TaskParams& tp);
+void build_task_params_raw(int BH, int H, int nseg, const int64_t* len, const uint32_t* kept,
+                           int rows_per_item, const int64_t* src_rows, const int64_t* dst_rows,
+                           TaskParams& tp);
 
 #define CK(x)                                                                        \
   do {                                                                               \
@@ -360,13 +363,71 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
         ++launches;
         return CQS_OK;
       };
-      // The first task has nothing to overlap its staging with, so it runs segment by segment as
-      // its data lands: after segment x arrives, one launch covers the kept (query, key) segment
-      // pairs whose later segment is x.  Splitting a task's key set over launches is exact: each
-      // launch LSE-merges its partial into the accumulator like a task (Eq. 3).
-      const bool split_first = run == 0 && __builtin_popcount(used) > 1;
-      uint32_t arrived = 0;
-      for (int a = 0; a < T.nseg; ++a) {
+      // The first task has nothing to overlap its staging with, so it runs piece by piece as its
+      // data lands: after piece x arrives, one launch covers the kept (query, key) piece pairs
+      // whose later piece is x.  Splitting a task's key set over launches is exact: each launch
+      // LSE-merges its partial into the accumulator like a task (Eq. 3).
+      const bool split_first = run == 0;
+      if (split_first) {
+        // pieces: every used segment cut into up to 4 consecutive row ranges (multiples of the
+        // 128-row tile, >= 2048 rows each) so the first launch waits for a quarter of a segment;
+        // a piece pair is kept iff its parent segments' pair is (pieces of one segment share its
+        // per-level codes, so the CQS mask is unchanged)
+        const int rpi = d.in_dtype == CQS_BF16 ? attn_rows_per_item(d.D) : 32;
+        const int nused = __builtin_popcount(used);
+        const int pmax = std::max(1, std::min(4, CQS_MAX_SEGS / nused));
+        int64_t pl[CQS_MAX_SEGS], ps[CQS_MAX_SEGS], psrc[CQS_MAX_SEGS], pdst[CQS_MAX_SEGS];
+        int par[CQS_MAX_SEGS], np = 0;
+        for (int a = 0; a < T.nseg; ++a) {
+          if (!(used >> a & 1)) continue;
+          const int64_t L = segs[a].len;
+          int k = int(std::min<int64_t>(pmax, std::max<int64_t>(1, L / 2048)));
+          const int64_t step = (L / k + 127) / 128 * 128;
+          for (int64_t o = 0; o < L; o += step) {
+            pl[np] = std::min(step, L - o);
+            ps[np] = segs[a].start + o;
+            psrc[np] = src[a] + o;
+            pdst[np] = dst[a] + o;
+            par[np] = a;
+            ++np;
+          }
+        }
+        uint32_t pk[CQS_MAX_SEGS] = {};
+        for (int x = 0; x < np; ++x)
+          for (int y = 0; y < np; ++y)
+            if (T.kept[par[x]] >> par[y] & 1) pk[x] |= 1u << y;
+        uint32_t arrived = 0;
+        for (int x = 0; x < np; ++x) {
+          for (int t = 0; t < 3; ++t)
+            CK(cudaMemcpy2DAsync(stage[b][t] + psrc[x] * D * e_in, size_t(Lh * D * e_in),
+                                 hq[t] + ps[x] * D * e_in, size_t(N * D * e_in),
+                                 size_t(pl[x] * D * e_in), size_t(BH), cudaMemcpyHostToDevice,
+                                 sc.cs));
+          h2d += uint64_t(3 * pl[x] * D * e_in * BH);
+          arrived |= 1u << x;
+          uint32_t kx[CQS_MAX_SEGS];
+          bool any = false;
+          for (int y = 0; y < np; ++y) {
+            kx[y] = y == x ? pk[y] & arrived : ((arrived >> y & 1) ? pk[y] & (1u << x) : 0u);
+            any |= kx[y] != 0;
+          }
+          if (!any) continue;
+          cudaEvent_t piece_ready = sc.ev();
+          CK(cudaEventRecord(piece_ready, sc.cs));
+          CK(cudaStreamWaitEvent(st, piece_ready, 0));
+          TaskParams tp;
+          build_task_params_raw(d.B * d.H, d.H, np, pl, kx, rpi, psrc, pdst, tp);
+          if (d.in_dtype == CQS_BF16)
+            CK(launch_attn_bf16(d.D, maps[b], tp, acc_o, acc_l, scale, st));
+          else
+            CK(launch_attn_f32(d.D, tp, reinterpret_cast<const float*>(stage[b][0]),
+                               reinterpret_cast<const float*>(stage[b][1]),
+                               reinterpret_cast<const float*>(stage[b][2]), sstr, acc_o, acc_l,
+                               scale, st));
+          ++launches;
+        }
+      }
+      for (int a = 0; a < T.nseg && !split_first; ++a) {
         if (!(used >> a & 1)) continue;
         for (int t = 0; t < 3; ++t)
           CK(cudaMemcpy2DAsync(stage[b][t] + src[a] * D * e_in, size_t(Lh * D * e_in),
@@ -374,28 +435,11 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
                                size_t(segs[a].len * D * e_in), size_t(BH),
                                cudaMemcpyHostToDevice, sc.cs));
         h2d += uint64_t(3 * segs[a].len * D * e_in * BH);
-        if (split_first) {
-          arrived |= 1u << a;
-          Task Tp = T;
-          bool any = false;
-          for (int x = 0; x < T.nseg; ++x) {
-            Tp.kept[x] = x == a ? T.kept[x] & arrived
-                                : ((arrived >> x & 1) ? T.kept[x] & (1u << a) : 0u);
-            any |= Tp.kept[x] != 0;
-          }
-          if (!any) continue;
-          cudaEvent_t seg_ready = sc.ev();
-          CK(cudaEventRecord(seg_ready, sc.cs));
-          CK(cudaStreamWaitEvent(st, seg_ready, 0));
-          cqs_status s2 = launch(Tp);
-          if (s2 != CQS_OK) return s2;
-        }
       }
       // The last task has nothing after it to overlap the output download with, so it runs query
-      // segment by query segment and each segment's final rows are downloaded while the next
-      // segment computes (device-tier accumulator only).
-      const bool split_last = j == 0 && !sharded && !split_first && ti == nmy - 1 &&
-                              [&] { int n = 0; for (int a = 0; a < T.nseg; ++a) n += T.kept[a] != 0; return n; }() > 1;
+      // piece by query piece (up to 4 per active query segment) and each piece's final rows are
+      // downloaded while the next piece computes (device-tier accumulator only).
+      const bool split_last = j == 0 && !sharded && !split_first && ti == nmy - 1;
       if (!split_first) {
         CK(cudaEventRecord(ev_ready[b], sc.cs));
         CK(cudaStreamWaitEvent(st, ev_ready[b], 0));
@@ -406,28 +450,53 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       }
       std::vector<std::pair<int64_t, int64_t>> rest;   // final rows of this task still to emit
       if (j == 0 && !sharded) rest = fin[size_t(ti)];
+      // query pieces of the last task (up to 4 per active query segment, multiples of the
+      // work-item rows): a piece's rows are downloaded while the next piece computes
+      const int rpi_l = d.in_dtype == CQS_BF16 ? attn_rows_per_item(d.D) : 32;
+      int64_t lq_len[CQS_MAX_SEGS], lq_src[CQS_MAX_SEGS], lq_dst[CQS_MAX_SEGS];
+      for (int x = 0; x < T.nseg; ++x)
+        lq_len[x] = segs[x].len, lq_src[x] = src[x], lq_dst[x] = dst[x];
       if (split_last)
         for (int a = 0; a < T.nseg; ++a) {
           if (!T.kept[a]) continue;
-          Task Tp = T;
-          for (int x = 0; x < T.nseg; ++x) Tp.kept[x] = x == a ? T.kept[x] : 0u;
-          cqs_status s2 = launch(Tp);
-          if (s2 != CQS_OK) return s2;
-          // rows of segment a whose last task is this one: emit them now, keep the remainder
-          const int64_t lo = segs[a].start, hi = segs[a].start + segs[a].len;
-          std::vector<std::pair<int64_t, int64_t>> keep;
-          for (const auto& iv : rest) {
-            const int64_t s0 = std::max(iv.first, lo), s1 = std::min(iv.first + iv.second, hi);
-            if (s0 >= s1) {
-              keep.push_back(iv);
-              continue;
+          const int npc = std::max(1, std::min<int>(4, CQS_MAX_SEGS - T.nseg));
+          const int64_t L = segs[a].len;
+          const int k = int(std::min<int64_t>(npc, std::max<int64_t>(1, L / 4096)));
+          const int64_t step = (L / k + rpi_l - 1) / rpi_l * rpi_l;
+          for (int64_t o = 0; o < L; o += step) {
+            // the piece is segment T.nseg (appended): query rows [o, o + len) of segment a
+            const int nq = T.nseg;
+            lq_len[nq] = std::min(step, L - o);
+            lq_src[nq] = src[a] + o;
+            lq_dst[nq] = dst[a] + o;
+            uint32_t kx[CQS_MAX_SEGS] = {};
+            kx[nq] = T.kept[a];
+            TaskParams tp;
+            build_task_params_raw(d.B * d.H, d.H, nq + 1, lq_len, kx, rpi_l, lq_src, lq_dst, tp);
+            if (d.in_dtype == CQS_BF16)
+              CK(launch_attn_bf16(d.D, maps[b], tp, acc_o, acc_l, scale, st));
+            else
+              CK(launch_attn_f32(d.D, tp, reinterpret_cast<const float*>(stage[b][0]),
+                                 reinterpret_cast<const float*>(stage[b][1]),
+                                 reinterpret_cast<const float*>(stage[b][2]), sstr, acc_o, acc_l,
+                                 scale, st));
+            ++launches;
+            // rows of this piece whose last task is this one: emit them now, keep the remainder
+            const int64_t lo = segs[a].start + o, hi = lo + lq_len[nq];
+            std::vector<std::pair<int64_t, int64_t>> keep;
+            for (const auto& iv : rest) {
+              const int64_t s0 = std::max(iv.first, lo), s1 = std::min(iv.first + iv.second, hi);
+              if (s0 >= s1) {
+                keep.push_back(iv);
+                continue;
+              }
+              cqs_status s2 = emit_rows(s0, s1 - s0);
+              if (s2 != CQS_OK) return s2;
+              if (iv.first < s0) keep.push_back({iv.first, s0 - iv.first});
+              if (s1 < iv.first + iv.second) keep.push_back({s1, iv.first + iv.second - s1});
             }
-            s2 = emit_rows(s0, s1 - s0);
-            if (s2 != CQS_OK) return s2;
-            if (iv.first < s0) keep.push_back({iv.first, s0 - iv.first});
-            if (s1 < iv.first + iv.second) keep.push_back({s1, iv.first + iv.second - s1});
+            rest.swap(keep);
           }
-          rest.swap(keep);
         }
       CK(cudaEventRecord(ev_free[b], st));
       buf_used[b] = true;
