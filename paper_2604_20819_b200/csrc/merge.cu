@@ -81,51 +81,80 @@ __device__ __forceinline__ void unit_weights(const MergeParts& parts, const floa
 }
 
 // One unit = one (row, plane) of D fp32 values.  min(32, D/4) lanes share a unit (one float4
-// column each, looping when D/4 > 32), so a warp covers 32 / lanes units per iteration; every
-// lane issues its NP part loads back to back (NP x 16 B in flight per lane) and the weights are
-// recomputed by each lane of the unit from broadcast lse loads.
+// column each, looping when D/4 > 32), so a warp covers 32 / lanes units per step; each lane
+// takes U units per iteration (U = 8 / (NP + 1) rounded down, >= 1) and issues all their
+// U x (NP + 1) 16-byte loads back to back, so even a 1-part merge keeps several loads in flight.
+// The weights are recomputed by each lane of a unit from broadcast lse loads.
 template <typename OutT, int NP, typename Idx>
 __global__ void __launch_bounds__(256)
     merge_kernel(Idx nunits, int BH, int H, int D4, MergeParts parts, float* __restrict__ acc_o,
                  float* __restrict__ acc_lse, bool acc_write, OutT* __restrict__ out, int64_t sB,
                  int64_t sH, int64_t sN, int64_t out_row0, int64_t n_total,
                  float* __restrict__ lse_out) {
+  constexpr int U = 8 / (NP + 1) > 1 ? 8 / (NP + 1) : 1;
   const int lane = threadIdx.x & 31;
   const int lpu = D4 < 32 ? D4 : 32, upw = 32 / lpu;
   const int lu = lane / lpu, sub = lane - lu * lpu;
   if (lu >= upw) return;
   const Idx warp0 = Idx((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5);
   const Idx nwarps = Idx((int64_t(gridDim.x) * blockDim.x) >> 5);
-  for (Idx unit = warp0 * upw + lu; unit < nunits; unit += nwarps * upw) {
-    float w[NP + 1];
-    float lse;
-    unit_weights<NP>(parts, acc_lse, int64_t(unit), w, lse);
-    const Idx r = unit / Idx(BH);
-    const int p = int(unit - r * Idx(BH));
-    const int bb = p / H, hh = p - bb * H;
+  const Idx gstep = Idx(upw) * U;
+  for (Idx g = warp0 * gstep; g < nunits; g += nwarps * gstep) {
+    float w[U][NP + 1];
+    float lse[U];
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const Idx unit = g + Idx(i * upw + lu);
+      if (unit < nunits) unit_weights<NP>(parts, acc_lse, int64_t(unit), w[i], lse[i]);
+    }
     for (int d4 = sub; d4 < D4; d4 += lpu) {
-      const int64_t f = int64_t(unit) * D4 + d4;
-      float4 x[NP + 1];
+      float4 x[U][NP + 1];
 #pragma unroll
-      for (int j = 0; j < NP; ++j)
-        if (w[j] != 0.f) x[j] = reinterpret_cast<const float4*>(parts.o[j])[f];
-      if (w[NP] != 0.f) x[NP] = reinterpret_cast<const float4*>(acc_o)[f];
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = 0; i < U; ++i) {
+        const Idx unit = g + Idx(i * upw + lu);
+        if (unit >= nunits) continue;
+        const int64_t f = int64_t(unit) * D4 + d4;
 #pragma unroll
-      for (int j = 0; j <= NP; ++j) {
-        if (w[j] == 0.f) continue;
-        v.x = fmaf(w[j], x[j].x, v.x);
-        v.y = fmaf(w[j], x[j].y, v.y);
-        v.z = fmaf(w[j], x[j].z, v.z);
-        v.w = fmaf(w[j], x[j].w, v.w);
+        for (int j = 0; j < NP; ++j)
+          if (w[i][j] != 0.f) x[i][j] = reinterpret_cast<const float4*>(parts.o[j])[f];
+        if (w[i][NP] != 0.f) x[i][NP] = reinterpret_cast<const float4*>(acc_o)[f];
       }
-      if (acc_write) reinterpret_cast<float4*>(acc_o)[f] = v;
-      if (out)
-        store4(out + int64_t(bb) * sB + int64_t(hh) * sH + (out_row0 + int64_t(r)) * sN + 4 * d4, v);
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const Idx unit = g + Idx(i * upw + lu);
+        if (unit >= nunits) continue;
+        const int64_t f = int64_t(unit) * D4 + d4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j <= NP; ++j) {
+          if (w[i][j] == 0.f) continue;
+          v.x = fmaf(w[i][j], x[i][j].x, v.x);
+          v.y = fmaf(w[i][j], x[i][j].y, v.y);
+          v.z = fmaf(w[i][j], x[i][j].z, v.z);
+          v.w = fmaf(w[i][j], x[i][j].w, v.w);
+        }
+        if (acc_write) reinterpret_cast<float4*>(acc_o)[f] = v;
+        if (out) {
+          const Idx r = unit / Idx(BH);
+          const int p = int(unit - r * Idx(BH));
+          const int bb = p / H, hh = p - bb * H;
+          store4(out + int64_t(bb) * sB + int64_t(hh) * sH + (out_row0 + int64_t(r)) * sN + 4 * d4,
+                 v);
+        }
+      }
     }
     if (sub == 0) {
-      if (acc_write) acc_lse[unit] = lse;
-      if (lse_out) lse_out[int64_t(p) * n_total + out_row0 + int64_t(r)] = lse;
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const Idx unit = g + Idx(i * upw + lu);
+        if (unit >= nunits) continue;
+        if (acc_write) acc_lse[unit] = lse[i];
+        if (lse_out) {
+          const Idx r = unit / Idx(BH);
+          const int p = int(unit - r * Idx(BH));
+          lse_out[int64_t(p) * n_total + out_row0 + int64_t(r)] = lse[i];
+        }
+      }
     }
   }
 }
