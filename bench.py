@@ -534,6 +534,9 @@ def main():
             host_qkv = make_host_qkv()
         hq, hk, hv = host_qkv
         sdesc = dict(desc_kw, qkv_loc="host", out_loc="host", schedule="uniform")
+        if world > 1:   # streamed plans are uniform trees: deep enough for >= 8 tasks per rank
+            while 7 ** sdesc["depth"] < 8 * world:
+                sdesc["depth"] += 1
         ps = cqs.cqs_plan(**sdesc)
         sdev, shost = cqs.cqs_forward_workspace_size(ps)
         if resident or sdev != dev_bytes:
@@ -608,7 +611,8 @@ def main():
                         if world == 1 else
                         "per rank: cqs_attention_forward streamed (its tasks' segments H2D from "
                         "a node-shared pinned Q/K/V), exchange, owned O / lse rows D2H"),
-               "acc_depth": ps.info().acc_depth, "stage_buffers": ps.info().n_stage_buffers}
+               "acc_depth": ps.info().acc_depth, "stage_buffers": ps.info().n_stage_buffers,
+               "depth": ps.info().depth}
         if world > 1:
             e2e["note"] = "h2d/d2h bytes are rank %d's; every rank moves its own share" % rank
         del sws, shws

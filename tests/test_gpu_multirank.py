@@ -24,7 +24,7 @@ def _free_port():
 
 
 def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo", schedule="uniform",
-            shard="lpt", qkv_loc="device"):
+            shard="lpt", qkv_loc="device", dtype="bf16"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import cqs_synth
@@ -34,11 +34,12 @@ def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo", schedule="un
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
-    q, k, v = cqs_synth.torch_qkv(1, H, N, D, 4242, dtype=torch.bfloat16, device="cuda")
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    q, k, v = cqs_synth.torch_qkv(1, H, N, D, 4242, dtype=tdt, device="cuda")
     streamed = qkv_loc == "host"
     if streamed:   # each rank stages only its tasks' segments from pinned host memory
         q, k, v = (t.cpu().pin_memory() for t in (q, k, v))
-    plan = cqs.cqs_plan(N=N, B=1, H=H, D=D, depth=depth, in_dtype="bf16", world=world, rank=rank,
+    plan = cqs.cqs_plan(N=N, B=1, H=H, D=D, depth=depth, in_dtype=dtype, world=world, rank=rank,
                         schedule=schedule, shard=shard, qkv_loc=qkv_loc,
                         out_loc="host" if streamed else "device")
     info = plan.info()
@@ -47,7 +48,7 @@ def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo", schedule="un
     ws = torch.empty(dev_bytes, dtype=torch.uint8, device="cuda")
     row0, rows = cqs.cqs_shard_rows(N, world, rank)
     assert info.shard_rows == rows
-    out = torch.zeros(1, H, rows, D, dtype=torch.bfloat16, device="cuda")   # owned shard only
+    out = torch.zeros(1, H, rows, D, dtype=tdt, device="cuda")   # owned shard only
     lse = torch.zeros(1, H, rows, dtype=torch.float32, device="cuda")
     cqs.cqs_attention_forward(plan, q, k, v, None, None, 0.0, 0, ws, None)
     torch.cuda.synchronize()
@@ -66,10 +67,11 @@ def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo", schedule="un
     dist.destroy_process_group()
 
 
-def _check_shards(tmp_path, world, N, H, D, seed=4242):
+def _check_shards(tmp_path, world, N, H, D, seed=4242, dtype=torch.bfloat16, tol=2e-2,
+                  ltol=1e-3):
     import cqs_synth
     from oracle import cqs_oracle as O
-    q, k, v = cqs_synth.torch_qkv(1, H, N, D, seed, dtype=torch.bfloat16)
+    q, k, v = cqs_synth.torch_qkv(1, H, N, D, seed, dtype=dtype)
     if N <= 6000:
         Od, ld = O.dense_attention(*(t.double().numpy() for t in (q, k, v)))
     rng = np.random.default_rng(N)
@@ -78,8 +80,11 @@ def _check_shards(tmp_path, world, N, H, D, seed=4242):
         o = np.load(tmp_path / ("o%d.npy" % r))
         l_ = np.load(tmp_path / ("l%d.npy" % r))
         if N <= 6000:
-            assert np.abs(o - Od[0, :, row0:row0 + rows]).max() <= 2e-2
-            assert np.abs(l_ - ld[0, :, row0:row0 + rows]).max() <= 1e-3
+            ref = Od[0, :, row0:row0 + rows]
+            err = np.abs(o - ref).max()
+            # bf16: absolute (R16); fp32: normwise relative (R15)
+            assert err <= (tol if dtype == torch.bfloat16 else tol * np.abs(ref).max()), err
+            assert np.abs(l_ - ld[0, :, row0:row0 + rows]).max() <= ltol
             continue
         # sampled rows: both shard edges plus random rows, every head
         sel = np.unique(np.concatenate([[0, rows - 1], rng.choice(rows, 150, replace=False)]))
@@ -175,3 +180,15 @@ def test_two_ranks_backward_one_gpu(N, depth, mode, schedule, tmp_path):
         for g, rf in zip(got, ref):
             rf = rf[0, :, row0:row0 + rows]
             assert np.linalg.norm(g - rf) / np.linalg.norm(rf) <= 1e-2
+
+
+@pytest.mark.parametrize("mode,shard,qkv_loc", [("p2p", "contiguous", "device"),
+                                                ("gloo", "lpt", "host")])
+def test_two_ranks_f32(mode, shard, qkv_loc, tmp_path):
+    """The fp32 path (BASELINE config 0's dtype) through the multi-rank data plane: rank-local
+    accumulators, streamed or resident, one exchange; R15 tolerance (1e-5 relative)."""
+    world, N, H, D, depth = 2, 1500, 2, 64, 2
+    mp.start_processes(_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path), mode,
+                                      "uniform", shard, qkv_loc, "f32"),
+                       nprocs=world, start_method="spawn")
+    _check_shards(tmp_path, world, N, H, D, dtype=torch.float32, tol=1e-5, ltol=1e-5)
