@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define CQS_ABI_VERSION 4
+#define CQS_ABI_VERSION 5
 #define CQS_MAX_DEPTH 12   /* N >= 7^depth and N < 2^31 imply depth <= 11 for c = 7           */
 #define CQS_MAX_SEGS 32    /* segments per task; observed <= 8 up to depth 11     */
 
@@ -101,6 +101,14 @@ typedef struct {
                                 CQS_E_INVALID if not a permutation of the planned task count
                                 (without CQS_PLAN_SUBSET) or not distinct valid indices.        */
   int64_t n_exec_order;
+  int32_t n_parallel;        /* tasks in flight ("n_parallel"): 0 or 1 = one task at a
+                                time on the caller's stream; P in [2, 8] (resident plans) = this
+                                rank's tasks round-robin over P streams, each with its own fp32
+                                accumulator slot (the in-place merge of one slot is never shared
+                                by concurrent tasks), merged into slot 0 at the end (Eq. 3).
+                                Costs (P - 1) extra accumulators in the memory model; pays off
+                                when single tasks do not fill the GPU (deep trees, few heads). */
+  int32_t reserved1;         /* must be 0                                                       */
 } cqs_plan_desc;
 
 #define CQS_SCHED_UNIFORM 0

@@ -59,8 +59,11 @@ def node_rows_max(N, c, I, j):
     return max(lens)
 
 
-def workspace_bytes(N, BH, D, e_in, streamed, out_host, staged_rows, acc_rows, nbuf):
+def workspace_bytes(N, BH, D, e_in, streamed, out_host, staged_rows, acc_rows, nbuf,
+                    n_parallel=1):
     b = _a256(acc_rows * BH * D * 4) + _a256(acc_rows * BH * 4)
+    if not streamed and n_parallel > 1:   # accumulator slots of concurrently running tasks
+        b += (n_parallel - 1) * (_a256(acc_rows * BH * D * 4) + _a256(acc_rows * BH * 4))
     if streamed:
         b += nbuf * 3 * _a256(BH * staged_rows * D * e_in)
     if streamed or out_host:
@@ -69,14 +72,15 @@ def workspace_bytes(N, BH, D, e_in, streamed, out_host, staged_rows, acc_rows, n
     return b
 
 
-def device_bytes(N, B, H, D, e_in, e_out, streamed, out_host, staged_rows, acc_rows, nbuf):
+def device_bytes(N, B, H, D, e_in, e_out, streamed, out_host, staged_rows, acc_rows, nbuf,
+                 n_parallel=1):
     """Each tensor as the caller's allocator holds it (_alloc, R14)."""
     BH = B * H
     caller = 0 if streamed else 3 * _alloc(BH * N * D * e_in)
     if not out_host:
         caller += _alloc(BH * N * D * e_out) + _alloc(4 * BH * N)
     return caller + _alloc(workspace_bytes(N, BH, D, e_in, streamed, out_host, staged_rows,
-                                          acc_rows, nbuf))
+                                          acc_rows, nbuf, n_parallel))
 
 
 def choose(N, B, H, D, e_in, e_out, streamed, out_host, budget, c=7, I=(0, 1, 3), depth=None,

@@ -56,7 +56,8 @@ class PlanDesc(C.Structure):
                 ("n_level_sets", C.c_int32), ("level_c", C.POINTER(C.c_int32)),
                 ("level_offsets", C.POINTER(C.c_int32)), ("shard", C.c_int32),
                 ("flags", C.c_int32), ("exec_order", C.POINTER(C.c_int64)),
-                ("n_exec_order", C.c_int64)]
+                ("n_exec_order", C.c_int64), ("n_parallel", C.c_int32),
+                ("reserved1", C.c_int32)]
 
 
 class PlanInfo(C.Structure):
@@ -162,11 +163,13 @@ def _loc_code(x):
 
 def make_desc(N, B, H, D, depth=1, budget_bytes=0, in_dtype="bf16", out_dtype=None,
               qkv_loc="device", out_loc=None, world=1, rank=0, c=7, offsets=(0, 1, 3),
-              schedule="uniform", levels=None, shard="lpt", exec_order=None, subset=False):
+              schedule="uniform", levels=None, shard="lpt", exec_order=None, subset=False,
+              n_parallel=0):
     """levels: optional [(c_t, offsets_t), ...] interest sets for divide levels 0, 1, ...
     (deeper levels use (c, offsets)).  shard: "lpt" | "contiguous" (world > 1 assignment).
     exec_order: optional permutation of the task indices (this rank's execution order); with
-    subset=True a list of distinct task indices: only those run (CQS_PLAN_SUBSET)."""
+    subset=True a list of distinct task indices: only those run (CQS_PLAN_SUBSET).
+    n_parallel: tasks in flight on separate streams / accumulator slots (resident plans)."""
     offs = (C.c_int32 * len(offsets))(*offsets)
     levels = list(levels or [])
     lc = (C.c_int32 * max(len(levels), 1))(*[int(c_t) for c_t, _ in levels])
@@ -182,7 +185,7 @@ def make_desc(N, B, H, D, depth=1, budget_bytes=0, in_dtype="bf16", out_dtype=No
                      schedule, schedule),
                  n_level_sets=len(levels), level_c=lc, level_offsets=lo,
                  shard={"lpt": CQS_SHARD_LPT, "contiguous": CQS_SHARD_CONTIGUOUS}.get(shard, shard),
-                 flags=CQS_PLAN_SUBSET if subset else 0)
+                 flags=CQS_PLAN_SUBSET if subset else 0, n_parallel=int(n_parallel), reserved1=0)
     eo = None
     if exec_order is not None:
         eo = (C.c_int64 * max(len(exec_order), 1))(*[int(x) for x in exec_order])

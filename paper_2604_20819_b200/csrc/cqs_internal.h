@@ -90,7 +90,7 @@ uint64_t align256(uint64_t x);
 uint64_t alloc_bytes(uint64_t x);
 // Section offsets of the device workspace (forward.cu must follow memory_model exactly).
 struct WsLayout {
-  uint64_t acc_o, acc_lse, stage, stage_bytes_per_buf, flush, total;
+  uint64_t acc_o, acc_lse, stage, stage_bytes_per_buf, flush, slots, slot_bytes, total;
 };
 WsLayout ws_layout(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_rows,
                    int32_t n_stage_buffers);

@@ -195,10 +195,20 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
     return fail(CQS_E_INVALID, "qkv strides: stride(D) must be 1");
   const int BH = d.B * d.H;
   const WsLayout L = ws_layout(d, 0, p->max_acc_rows, 0);
-  float* acc_o = reinterpret_cast<float*>(ws + L.acc_o);
-  float* acc_lse = reinterpret_cast<float*>(ws + L.acc_lse);
+  // n_parallel > 1: slot s in [0, P) = stream s (0 = the caller's) + its own accumulator
+  const int P = std::max(1, int(d.n_parallel));
+  std::vector<float*> slot_o(static_cast<size_t>(P)), slot_l(static_cast<size_t>(P));
+  for (int s = 0; s < P; ++s) {
+    uint8_t* base = s == 0 ? ws : ws + L.slots + uint64_t(s - 1) * L.slot_bytes;
+    slot_o[size_t(s)] = reinterpret_cast<float*>(base + (s == 0 ? L.acc_o : 0));
+    slot_l[size_t(s)] = reinterpret_cast<float*>(
+        base + (s == 0 ? L.acc_lse : align256(uint64_t(p->max_acc_rows) * BH * d.D * 4)));
+  }
+  float* acc_o = slot_o[0];
+  float* acc_lse = slot_l[0];
   int64_t launches = 0;
-  // stats: CUDA events around every launch on `st` (kernel durations, not host time)
+  // stats: CUDA events around every launch on `st` (kernel durations, not host time); with P > 1
+  // one pair around all tasks (they overlap across streams)
   std::vector<cudaEvent_t> evs;
   auto mark = [&]() {
     if (!stats) return;
@@ -208,10 +218,35 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
     evs.push_back(ev);
   };
   mark();
-  cudaError_t e = launch_fill(acc_lse, p->max_acc_rows * BH, -INFINITY, st);
+  cudaError_t e = cudaSuccess;
+  for (int s = 0; s < P && e == cudaSuccess; ++s, ++launches)
+    e = launch_fill(slot_l[size_t(s)], p->max_acc_rows * BH, -INFINITY, st);
   mark();
-  ++launches;
   if (e != cudaSuccess) return fail(CQS_E_CUDA, cudaGetErrorString(e));
+  struct Streams {   // helper streams + events of the P > 1 mode, released on every return path
+    std::vector<cudaStream_t> s;
+    std::vector<cudaEvent_t> e;
+    ~Streams() {
+      for (auto x : e) cudaEventDestroy(x);
+      for (auto x : s) cudaStreamDestroy(x);
+    }
+  } ps;
+  std::vector<cudaStream_t> sts(size_t(P), st);
+  if (P > 1) {
+    cudaEvent_t filled;
+    if ((e = cudaEventCreateWithFlags(&filled, cudaEventDisableTiming)) != cudaSuccess)
+      return fail(CQS_E_CUDA, cudaGetErrorString(e));
+    ps.e.push_back(filled);
+    cudaEventRecord(filled, st);
+    for (int s = 1; s < P; ++s) {
+      cudaStream_t x;
+      if ((e = cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(CQS_E_CUDA, cudaGetErrorString(e));
+      ps.s.push_back(x);
+      sts[size_t(s)] = x;
+      cudaStreamWaitEvent(x, filled, 0);
+    }
+  }
 
   CUtensorMap maps[3];
   if (d.in_dtype == CQS_BF16) {
@@ -228,28 +263,53 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
   int64_t run = 0;
   for (int64_t ti : p->my_order) {
     const Task& T = p->tasks[size_t(ti)];
+    const int slot = int(run % P);
     auto seg_start = [&](int a) { return p->segs[size_t(T.seg_off + a)].start; };
     auto seg_acc = [&](int a) { return p->acc_row(p->segs[size_t(T.seg_off + a)].start); };
     build_task_params(p, T, rows_per_item, seg_start, seg_acc, tp);
-    mark();
+    if (P == 1) mark();
+    cudaStream_t ts = sts[size_t(slot)];
     if (d.in_dtype == CQS_BF16)
-      e = launch_attn_bf16(d.D, maps, tp, acc_o, acc_lse, scale, st);
+      e = launch_attn_bf16(d.D, maps, tp, slot_o[size_t(slot)], slot_l[size_t(slot)], scale, ts);
     else
       e = launch_attn_f32(d.D, tp, static_cast<const float*>(q), static_cast<const float*>(k),
-                          static_cast<const float*>(v), qkv_strides, acc_o, acc_lse, scale, st);
-    mark();
+                          static_cast<const float*>(v), qkv_strides, slot_o[size_t(slot)],
+                          slot_l[size_t(slot)], scale, ts);
+    if (P == 1) mark();
     if (e != cudaSuccess) return fail(CQS_E_CUDA, std::string("attention launch: ") + cudaGetErrorString(e));
     ++launches;
     ++run;
   }
+  if (P > 1) {   // join the helper streams, then fold slots 1..P-1 into slot 0 (Eq. 3)
+    for (int s = 1; s < P; ++s) {
+      cudaEvent_t done;
+      if ((e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming)) != cudaSuccess)
+        return fail(CQS_E_CUDA, cudaGetErrorString(e));
+      ps.e.push_back(done);
+      cudaEventRecord(done, sts[size_t(s)]);
+      cudaStreamWaitEvent(st, done, 0);
+    }
+    mark();
+    if (d.world > 1) {   // the exchange reads slot 0: merge the others into it in place
+      e = launch_merge(p->max_acc_rows, d.B, d.H, d.D, P - 1, slot_o.data() + 1,
+                       slot_l.data() + 1, acc_o, acc_lse, true, nullptr, d.out_dtype, nullptr, 0,
+                       p->max_acc_rows, nullptr, st);
+      ++launches;
+      if (e != cudaSuccess) return fail(CQS_E_CUDA, std::string("slot merge: ") + cudaGetErrorString(e));
+    }
+  }
   const auto t1 = std::chrono::steady_clock::now();
   if (d.world == 1) {
-    mark();
-    e = launch_merge(d.N, d.B, d.H, d.D, 0, nullptr, nullptr, acc_o, acc_lse, false, out,
+    if (P == 1) mark();
+    // finalize (P > 1: the slots' merge and the finalize in one kernel)
+    e = launch_merge(d.N, d.B, d.H, d.D, P - 1, P > 1 ? slot_o.data() + 1 : nullptr,
+                     P > 1 ? slot_l.data() + 1 : nullptr, acc_o, acc_lse, false, out,
                      d.out_dtype, out_strides, 0, d.N, lse, st);
     mark();
     ++launches;
     if (e != cudaSuccess) return fail(CQS_E_CUDA, std::string("finalize: ") + cudaGetErrorString(e));
+  } else if (P > 1) {
+    mark();
   }
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
@@ -258,11 +318,13 @@ extern "C" cqs_status cqs_attention_forward(const cqs_plan_t* p, const void* q, 
     const auto t2 = std::chrono::steady_clock::now();
     stats->ms_total = std::chrono::duration<double, std::milli>(t2 - t0).count();
     (void)t1;
-    // pairs: [fill] [task_0] ... [task_{run-1}] [finalize]
+    // P = 1 pairs: [fill] [task_0] ... [task_{run-1}] [finalize];  P > 1: [fill] [all tasks]
+    // [merge + finalize]
+    const size_t n_attn = P == 1 ? size_t(run) : 1;
     for (size_t i = 0; i + 1 < evs.size(); i += 2) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, evs[i], evs[i + 1]);
-      const bool is_attn = i >= 2 && i < 2 + 2 * size_t(run);
+      const bool is_attn = i >= 2 && i < 2 + 2 * n_attn;
       (is_attn ? stats->ms_attn : stats->ms_merge) += ms;
     }
     for (auto ev : evs) cudaEventDestroy(ev);

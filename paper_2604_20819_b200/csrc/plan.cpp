@@ -62,6 +62,11 @@ WsLayout ws_layout(const cqs_plan_desc& d, int64_t staged_rows, int64_t acc_rows
     const uint64_t F = uint64_t(flush_rows(acc_rows, int64_t(BH), int64_t(D)));
     off += 2 * (align256(F * BH * D * 4) + align256(F * BH * 4));
   }
+  // n_parallel > 1 (resident): accumulator slots 1..P-1 for concurrently running tasks
+  w.slots = off;
+  w.slot_bytes = align256(uint64_t(acc_rows) * BH * D * 4) + align256(uint64_t(acc_rows) * BH * 4);
+  if (d.qkv_loc == CQS_LOC_DEVICE && d.n_parallel > 1)
+    off += uint64_t(d.n_parallel - 1) * w.slot_bytes;
   w.total = off;
   return w;
 }
@@ -475,6 +480,11 @@ static cqs_status validate_desc(const cqs_plan_desc* d, Levels& lv) {
   if (d->shard != CQS_SHARD_LPT && d->shard != CQS_SHARD_CONTIGUOUS)
     return fail(CQS_E_INVALID, "shard must be CQS_SHARD_LPT or CQS_SHARD_CONTIGUOUS");
   if (d->flags & ~CQS_PLAN_SUBSET) return fail(CQS_E_INVALID, "unknown flags");
+  if (d->reserved1 != 0) return fail(CQS_E_INVALID, "reserved1 must be 0");
+  if (d->n_parallel < 0 || d->n_parallel > 8) return fail(CQS_E_INVALID, "n_parallel in [0, 8]");
+  if (d->n_parallel > 1 && d->qkv_loc != CQS_LOC_DEVICE)
+    return fail(CQS_E_UNSUPPORTED, "n_parallel > 1: resident plans only (the streamed executor "
+                                   "overlaps staging with one task at a time)");
   if ((d->flags & CQS_PLAN_SUBSET) && !d->exec_order)
     return fail(CQS_E_INVALID, "CQS_PLAN_SUBSET needs exec_order");
   if (d->n_exec_order < 0 || (d->n_exec_order > 0 && !d->exec_order))

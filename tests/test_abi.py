@@ -18,7 +18,7 @@ def test_header_symbols_exported():
     L = ctypes.CDLL(cqs.LIB_PATH)
     for name in declared:
         assert hasattr(L, name), name
-    assert cqs.lib().cqs_abi_version() == 4
+    assert cqs.lib().cqs_abi_version() == 5
 
 
 def test_struct_sizes_match_c_layout(tmp_path):

@@ -265,3 +265,25 @@ def test_subset_calls_merge_to_full_attention(streamed):
     cqs.cqs_merge(N, B, H, D, [r[0] for r in res], [r[1] for r in res], out=fo, lse_out=fl)
     torch.cuda.synchronize()
     check_bf16(fo, fl, *ref_dense(q, k, v))
+
+
+@pytest.mark.parametrize("P,N,depth,D", [(2, 3000, 2, 128), (4, 2401, 3, 64), (8, 5000, 4, 128),
+                                         (3, 1030, 2, 64)])
+def test_parallel_task_slots(P, N, depth, D):
+    """n_parallel = P: tasks round-robin over P streams, each with its own accumulator
+    slot, folded together at the end — equals dense attention, and differs from the one-stream
+    result only by fp rounding."""
+    q, k, v = gen(1, 2, N, D, 700 + P + N, bf16=True)
+    res = []
+    for n_par in (1, P):
+        p = cqs.cqs_plan(N=N, B=1, H=2, D=D, depth=depth, n_parallel=n_par)
+        ws = torch.empty(cqs.cqs_forward_workspace_size(p)[0], dtype=torch.uint8, device=DEV)
+        out = torch.empty_like(q)
+        lse = torch.empty(1, 2, N, dtype=torch.float32, device=DEV)
+        st = cqs.cqs_attention_forward(p, q, k, v, out, lse, 0.0, 0, ws, None, stats=True)
+        torch.cuda.synchronize()
+        assert st.tasks_run == p.info().my_tasks
+        res.append((out.clone(), lse.clone()))
+    check_bf16(*res[1], *ref_dense(q, k, v))
+    assert (res[0][0].float() - res[1][0].float()).abs().max().item() <= 1e-2
+    assert (res[0][1] - res[1][1]).abs().max().item() <= 1e-5

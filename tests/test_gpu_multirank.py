@@ -24,7 +24,7 @@ def _free_port():
 
 
 def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo", schedule="uniform",
-            shard="lpt", qkv_loc="device", dtype="bf16"):
+            shard="lpt", qkv_loc="device", dtype="bf16", n_parallel=0):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import cqs_synth
@@ -41,7 +41,7 @@ def _worker(rank, world, port, N, H, D, depth, outdir, mode="gloo", schedule="un
         q, k, v = (t.cpu().pin_memory() for t in (q, k, v))
     plan = cqs.cqs_plan(N=N, B=1, H=H, D=D, depth=depth, in_dtype=dtype, world=world, rank=rank,
                         schedule=schedule, shard=shard, qkv_loc=qkv_loc,
-                        out_loc="host" if streamed else "device")
+                        out_loc="host" if streamed else "device", n_parallel=n_parallel)
     info = plan.info()
     dev_bytes, host_bytes = cqs.cqs_forward_workspace_size(plan)
     assert host_bytes == 0
@@ -192,3 +192,13 @@ def test_two_ranks_f32(mode, shard, qkv_loc, tmp_path):
                                       "uniform", shard, qkv_loc, "f32"),
                        nprocs=world, start_method="spawn")
     _check_shards(tmp_path, world, N, H, D, dtype=torch.float32, tol=1e-5, ltol=1e-5)
+
+
+def test_two_ranks_parallel_slots(tmp_path):
+    """world 2 with 3 tasks in flight per rank: the slots are folded into the rank-local
+    accumulator before the exchange reads it."""
+    world, N, H, D, depth = 2, 3000, 2, 128, 3
+    mp.start_processes(_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path), "p2p",
+                                      "uniform", "contiguous", "device", "bf16", 3),
+                       nprocs=world, start_method="spawn")
+    _check_shards(tmp_path, world, N, H, D)

@@ -89,3 +89,12 @@ def test_backward_workspace_matches_c_abi(N, B, H, D):
     assert one < two
     if N == 14458261:   # the C5 scaled backward under 16 GiB takes one staging buffer (14.43 GB)
         assert one <= 16 << 30 < two
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_parallel_slots_bytes(P):
+    """n_parallel > 1 (resident): one extra fp32 accumulator per additional task in flight."""
+    N, B, H, D = 50000, 1, 4, 128
+    p = cqs.cqs_plan(N=N, B=B, H=H, D=D, depth=2, n_parallel=P)
+    assert p.info().predicted_peak_bytes == M.device_bytes(N, B, H, D, 2, 2, False, False, 0, N,
+                                                          0, n_parallel=P)
