@@ -97,3 +97,25 @@ def test_subset_plan_runs_only_listed_tasks():
     assert p.info().my_work_pairs == w
     with pytest.raises(cqs.CqsError):
         cqs.cqs_plan(N=500, B=1, H=1, D=128, depth=2, exec_order=[40, 40], subset=True)
+
+
+def test_exchange_merge_argument_errors():
+    """cqs_exchange_merge rejects world-1 plans and NULL parts before touching the device."""
+    import ctypes
+    p = cqs.cqs_plan(N=500, B=1, H=1, D=128, depth=1)
+    P = ctypes.c_void_p
+    st = cqs.lib().cqs_exchange_merge(p.handle, (P * 1)(), (P * 1)(), (ctypes.c_int64 * 1)(), None,
+                                      None, None, None)
+    assert st == cqs.CQS_E_INVALID
+    p2 = cqs.cqs_plan(N=500, B=1, H=1, D=128, depth=1, world=2, rank=0)
+    strides = (ctypes.c_int64 * 4)(500 * 128, 500 * 128, 128, 1)
+    st = cqs.lib().cqs_exchange_merge(p2.handle, (P * 2)(None, None), (P * 2)(None, None),
+                                      (ctypes.c_int64 * 2)(0, 0), P(1 << 20), strides, None, None)
+    assert st == cqs.CQS_E_INVALID and b"NULL" in cqs.lib().cqs_last_error()
+
+
+def test_partial_runs_identity_at_world_one():
+    p = cqs.cqs_plan(N=1000, B=1, H=1, D=128, depth=2)
+    assert cqs.cqs_partial_runs(p, 0, 100, 50) == [(100, 50, 100)]
+    with pytest.raises(cqs.CqsError):
+        cqs.cqs_partial_runs(p, 1, 0, 10)
