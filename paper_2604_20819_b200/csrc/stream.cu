@@ -51,6 +51,13 @@ void build_task_params_raw(int BH, int H, int nseg, const int64_t* len, const ui
     if (e_ != cudaSuccess) return fail(CQS_E_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
   } while (0)
 
+// Pieces per segment of the first task (staged and launched as they land) and per active query
+// segment of the last task (downloaded while the next piece computes).  Measured on C2 e2e: one
+// piece per segment 263 ms / step, four pieces 275 ms (each extra launch of a partial block adds a
+// wave-quantisation tail that costs more than the shorter fill / drain saves).
+constexpr int kFirstPieces = 1;
+constexpr int kLastPieces = 1;
+
 namespace {
 struct Scoped {
   cudaStream_t cs = nullptr, fh = nullptr, fd = nullptr;
@@ -375,7 +382,7 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
         // per-level codes, so the CQS mask is unchanged)
         const int rpi = d.in_dtype == CQS_BF16 ? attn_rows_per_item(d.D) : 32;
         const int nused = __builtin_popcount(used);
-        const int pmax = std::max(1, std::min(4, CQS_MAX_SEGS / nused));
+        const int pmax = std::max(1, std::min(kFirstPieces, CQS_MAX_SEGS / nused));
         int64_t pl[CQS_MAX_SEGS], ps[CQS_MAX_SEGS], psrc[CQS_MAX_SEGS], pdst[CQS_MAX_SEGS];
         int par[CQS_MAX_SEGS], np = 0;
         for (int a = 0; a < T.nseg; ++a) {
@@ -459,7 +466,7 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       if (split_last)
         for (int a = 0; a < T.nseg; ++a) {
           if (!T.kept[a]) continue;
-          const int npc = std::max(1, std::min<int>(4, CQS_MAX_SEGS - T.nseg));
+          const int npc = std::max(1, std::min<int>(kLastPieces, CQS_MAX_SEGS - T.nseg));
           const int64_t L = segs[a].len;
           const int k = int(std::min<int64_t>(npc, std::max<int64_t>(1, L / 4096)));
           const int64_t step = (L / k + rpi_l - 1) / rpi_l * rpi_l;

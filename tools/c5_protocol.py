@@ -90,6 +90,9 @@ def main():
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--window", type=int, default=49, help="0 = skip the contiguous window")
     ap.add_argument("--rows", type=int, default=2, help="parity rows per batch")
+    ap.add_argument("--first-batch", type=int, default=0,
+                    help="run the sample from this batch index on (resume a cut-off run: the "
+                         "sample is seeded, so batches are reproducible)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -226,12 +229,13 @@ def main():
                       p=works[nonempty] / works[nonempty].sum())
     pick = np.sort(pick)
     batches = []
-    for i in range(0, len(pick), args.batch):
-        batches.append(run(pick[i:i + args.batch], "sample batch %d" % (i // args.batch), rng))
+    for i in range(args.first_batch * args.batch, len(pick), args.batch):
+        batches.append(run(pick[i:i + args.batch], "sample batch %d" % (i // args.batch),
+                           np.random.default_rng(seed + 1 + i // args.batch)))
     res["sample"] = batches
     s_flop = sum(b["useful_flop"] for b in batches)
     s_ms = sum(b["ms"] for b in batches)
-    rate = s_flop / (s_ms * 1e-3)
+    rate = s_flop / (s_ms * 1e-3) if batches else float("nan")
     res["sample_rate_tflops"] = rate / 1e12
     if args.window:
         # all leaves under one depth-(k-2) node (49 leaves when k >= 2), DFS-contiguous; chosen at
@@ -239,9 +243,10 @@ def main():
         span = 7 ** 2 if k >= 2 else nt
         n0 = int(rng.integers(nt // span)) * span
         win = [t for t in range(n0, n0 + span) if works[t] > 0][:args.window]
-        res["window"] = run(win, "window: tasks %d..%d" % (n0, n0 + span - 1), rng)
+        res["window"] = run(win, "window: tasks %d..%d" % (n0, n0 + span - 1),
+                            np.random.default_rng(seed + 999))
     total_flop = 4.0 * N * N * D * H
-    res["extrapolated_full_pass_h"] = total_flop / rate / 3600
+    res["extrapolated_full_pass_h"] = total_flop / rate / 3600 if batches else None
     if args.window:
         res["extrapolated_full_pass_h_window_rate"] = total_flop / (
             res["window"]["tflops"] * 1e12) / 3600
