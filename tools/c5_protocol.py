@@ -183,12 +183,16 @@ def main():
         torch.cuda.synchronize()
         t_gen = time.time() - t_gen
         p = cqs.cqs_plan(exec_order=tasks, subset=True, **desc)
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats()   # the call's own bytes, not the generator's
+        a0 = torch.cuda.memory_allocated()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         st = cqs.cqs_attention_forward(p, q, kk, v, o, lse, 0.0, budget, ws, hws, stats=True)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
+        call_peak = torch.cuda.max_memory_allocated() - a0 + ws.numel()
         work = float(sum(T.work for T, _, _ in info_t))
         # parity rows: query rows of active segments; reference over the union of their kept keys
         errs, lerrs = [], []
@@ -217,6 +221,7 @@ def main():
              "bytes_h2d": st.bytes_h2d, "bytes_d2h": st.bytes_d2h,
              "h2d_gbs_avg": st.bytes_h2d / (ms * 1e-3) / 1e9,
              "kernel_launches": st.kernel_launches, "host_gb_touched": sum(n for _, n in pages) / 1e9,
+             "device_bytes_during_call": call_peak,
              "register_s": t_reg, "generate_s": t_gen,
              "parity_max_abs_err": max(errs), "parity_max_lse_err": max(lerrs),
              "parity_ok": max(errs) <= 2e-2 and max(lerrs) <= 1e-3}
