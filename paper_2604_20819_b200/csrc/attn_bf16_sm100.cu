@@ -73,21 +73,11 @@ struct AttnCfg {
 #endif
   static constexpr int kStages = D == 128 ? 4 : CQS_ONE_STAGES64;
   static constexpr int kSmemBytes = 2 * kQBytes + kStages * kKVBytes + 1024 + 512;
-#ifdef CQS_D64_SEPP
-  // separate P region (D = 64): S_t(j+1) is issued as soon as the softmax has read S_t(j) into
-  // registers, so the next S overlaps the current exp pass instead of following PV_t(j); Q then
-  // stays in SMEM (S0 | S1 | P0 | P1 | O0 | O1 = 128 + 128 + 64 + 64 + 64 + 64 columns)
-  static constexpr bool kSepP = D == 64;
-#else
-  static constexpr bool kSepP = false;
-#endif
-  static constexpr uint32_t kColS0 = 0, kColS1 = 128;
-  static constexpr uint32_t kColO0 = kSepP ? 384 : 256, kColO1 = kSepP ? 448 : 256 + D;
-  static constexpr uint32_t kColP0 = kSepP ? 256 : kColS0, kColP1 = kSepP ? 320 : kColS1;
+  static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 256 + D;
   // D = 64: Q lives in TMEM (A operand of S = Q K^T from TMEM, kind::f16 packed like P), so the
   // S MMA reads only K from shared memory (an SS MMA at M = N = 128 needs the full 128 B/clk of
   // SMEM bandwidth, leaving none for the TMA fills).  D = 128 has no free TMEM columns for it.
-  static constexpr bool kQInTmem = D == 64 && !kSepP;
+  static constexpr bool kQInTmem = D == 64;
   static constexpr uint32_t kColQ0 = 256 + 2 * D, kColQ1 = 256 + 2 * D + D / 2;
 };
 
@@ -112,8 +102,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t* p_full = s_full + 2;              // 2
   uint64_t* o_bar = p_full + 2;               // 2
   uint64_t* q_tm = o_bar + 2;                 // 1: Q copied into TMEM (kQInTmem)
-  uint64_t* s_free = q_tm + 1;                // 2: S_t read into registers (kSepP)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_tm + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -145,7 +134,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       ptx::mbar_init(&s_full[t], 1);
       ptx::mbar_init(&p_full[t], 4);
       ptx::mbar_init(&o_bar[t], 1);
-      ptx::mbar_init(&s_free[t], 4);
     }
     ptx::mbar_init(q_tm, two ? 8 : 4);
     ptx::fence_barrier_init();
@@ -223,7 +211,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       };
       auto issue_PV = [&](int t, int s, bool acc) {
         const uint64_t vb = dv0 + uint64_t((s * C::kKVBytes) >> 4);
-        const uint32_t d = tmem + (t ? C::kColO1 : C::kColO0), pa = tmem + (t ? C::kColP1 : C::kColP0);
+        const uint32_t d = tmem + (t ? C::kColO1 : C::kColO0), pa = tmem + (t ? C::kColS1 : C::kColS0);
 #pragma unroll
         for (int ks = 0; ks < kBN / 16; ++ks)
           ptx::mma_ts_elect(d, pa + ks * 8, vb + uint64_t((ks * 16 * 128) >> 4), idesc_pv,
@@ -249,28 +237,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           sKn = it % C::kStages;
           ptx::mbar_wait(&kv_full[sKn], (it / C::kStages) & 1);
           ++it;
-        }
-        if constexpr (C::kSepP) {
-          // S_t(j+1) as soon as the softmax has read S_t(j); PV_t(j) once P_t(j) is written
-          if (sKn >= 0) {
-            for (int t = 0; t < (two ? 2 : 1); ++t) {
-              ptx::mbar_wait(&s_free[t], j & 1);
-              ptx::tc_fence_after();
-              issue_S(t, sKn);
-            }
-            ptx::mma_commit_elect(&kv_empty[sKn]);
-          }
-          const int sVp = it % C::kStages;
-          ptx::mbar_wait(&kv_full[sVp], (it / C::kStages) & 1);
-          ++it;
-          ptx::tc_fence_after();
-          for (int t = 0; t < (two ? 2 : 1); ++t) {
-            ptx::mbar_wait(&p_full[t], j & 1);
-            ptx::tc_fence_after();
-            issue_PV(t, sVp, j > 0);
-          }
-          ptx::mma_commit_elect(&kv_empty[sVp]);
-          continue;
         }
         const int sV = it % C::kStages;
         DBG1_T0(tk0);
@@ -313,7 +279,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t lane_base = uint32_t(sub * 32) << 16;
       const uint32_t tS = tmem + lane_base + (t ? C::kColS1 : C::kColS0);
       const uint32_t tO = tmem + lane_base + (t ? C::kColO1 : C::kColO0);
-      const uint32_t tP = tmem + lane_base + (t ? C::kColP1 : C::kColP0);
       float m = -INFINITY, l = 0.f;
       if constexpr (C::kQInTmem) {
         // this thread's Q row (SW128 TMA box: 16-byte chunk c of row r sits at chunk c ^ (r & 7))
@@ -347,17 +312,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int c = 0; c < kBN / 32; ++c)
           ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
         ptx::tmem_ld_wait();
-        if constexpr (C::kSepP) {
-          // S_t(j) is in registers: the MMA warp may compute S_t(j+1) into the S columns now;
-          // P_t(j) goes to its own columns once PV_t(j-1) has read P_t(j-1)
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&s_free[t]);
-          if (j > 0) {
-            ptx::mbar_wait(&o_bar[t], (j - 1) & 1);
-            ptx::tc_fence_after();
-          }
-        }
         float* s = reinterpret_cast<float*>(sr);
         if (valid < kBN) {
 #pragma unroll
@@ -400,7 +354,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
               rs2[ii & 3] = ptx::fadd2(rs2[ii & 3], ptx::f2(x0, x1));
               pk[ii] = ptx::pack_bf16(x0, x1);
             }
-            ptx::tmem_st16(tP + c * 16, pk);
+            ptx::tmem_st16(tS + c * 16, pk);
           }
           if (kTrack) rmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
           const uint64_t rr = ptx::fadd2(ptx::fadd2(rs2[0], rs2[1]), ptx::fadd2(rs2[2], rs2[3]));
