@@ -39,6 +39,13 @@ __device__ unsigned long long g_cqs_dbg1[16];
 #define DBG1_T0(v)
 #define DBG1_ADD(i, x) ((void)0)
 #endif
+// P stored to TMEM after the whole exp pass (two x32 stores) instead of one x16 store per
+// 32-column chunk: the chunked stores' source registers are re-used by the next chunk's packs,
+// so every chunk waits until its tcgen05.st has read them (WAR on the STTM operands).
+#ifndef CQS_PST_END
+#define CQS_PST_END 0
+#endif
+constexpr bool kPstEnd = CQS_PST_END != 0;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
 // setmaxnreg split (see the register note in the kernel): 4 warps at LO, 8 softmax warps at HI
 // (56 / 224: no spills; measured +3.9% over 72 / 216 at D = 64: 725 vs 697 TFLOP/s, 3 runs each)
@@ -58,10 +65,14 @@ template <int D> constexpr uint32_t kPolyMask = CQS_DBG_POLY_MASK;
 template <int D> constexpr uint32_t kPolyMask = 0x0;
 #endif
 
-// Warpgroup ping-pong of the two tiles' softmax phases (named barriers 1 / 2).  Off: measured
-// slower at both head dims (D = 64: 651 vs 735 TFLOP/s; cycle counters in profiles/r01_notes.md).
+// Sequenced exp passes of the two tiles (named barriers 1 / 2, 8 warps each): each tile's pass
+// runs alone on its sub-partition's MUFU; the S load (tcgen05.ld) stays outside the sequenced
+// region.  (Round 1 sequenced the whole phase including the S load: 651 vs 735 TFLOP/s.)
+#ifndef CQS_ONE_SEQ
+#define CQS_ONE_SEQ 0
+#endif
 template <int D>
-constexpr bool kPingPong = false;
+constexpr bool kPingPong = CQS_ONE_SEQ != 0;
 
 template <int D>
 struct AttnCfg {
@@ -166,6 +177,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const int s = it % C::kStages;
         const uint32_t ph = (it / C::kStages) & 1;
         ptx::mbar_wait(&kv_empty[s], ph ^ 1);
+#ifdef CQS_DBG_NO_REFILL   // diagnostic only (wrong results): stages loaded once, then reused
+        if (it >= C::kStages) {
+          ptx::mbar_arrive(&kv_full[s]);
+          ++it;
+          return;
+        }
+#endif
         ptx::mbar_arrive_expect_tx(&kv_full[s], C::kKVBytes);
         for (int bx = 0; bx < C::kBoxes; ++bx)
           ptx::tma_load_4d(sKV + s * C::kKVBytes + bx * kBN * 128, map, &kv_full[s], bx * 64, row,
@@ -306,7 +324,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         ptx::mbar_wait(&s_full[t], j & 1);
         ptx::tc_fence_after();
         DBG1_T0(ts1);
-        if (kPingPong<D> && two && !(t == 0 && j == 0)) ptx::named_bar_sync(1 + t, 256);
         uint32_t sr[kBN];
 #pragma unroll
         for (int c = 0; c < kBN / 32; ++c)
@@ -318,6 +335,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           for (int c = 0; c < kBN; ++c)
             if (c >= valid) s[c] = -INFINITY;
         }
+        if (kPingPong<D> && two && !(t == 0 && j == 0)) ptx::named_bar_sync(1 + t, 256);
         // One exp2 pass: p = 2^(s*scale_log2 - m_use) (packed FFMA2 argument, MUFU.EX2 — or the
         // FMA-pipe polynomial for the pairs in kPolyMask), fused per 32-column chunk with the
         // packed row sum, the bf16 pack and the tcgen05.st of P.  With TRACK it also takes the
@@ -331,9 +349,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) mx4[u] = -INFINITY;
           }
+          uint32_t pka[kBN / 2];   // packed bf16 P of the whole row
 #pragma unroll
           for (int c = 0; c < kBN / 32; ++c) {
-            uint32_t pk[16];
+            uint32_t(&pk)[16] = *reinterpret_cast<uint32_t(*)[16]>(&pka[16 * c]);
 #pragma unroll
             for (int ii = 0; ii < 16; ++ii) {
               const int i = 16 * c + ii;
@@ -342,19 +361,30 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                                           fmaxf(fmaxf(s[2 * i], s[2 * i + 1]),
                                                 fmaxf(s[2 * i + 2], s[2 * i + 3])));
               float x0, x1;
+#ifdef CQS_DBG_NO_EXP   // diagnostic only (wrong results): P = raw S, no exponentials
+              x0 = s[2 * i], x1 = s[2 * i + 1];
+              if (false) {
+#else
               ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
               if ((kPolyMask<D> >> (i & 7)) & 1) {
+#endif
                 ptx::exp2_poly_pair(x0, x1);
                 if (2 * i >= valid) x0 = 0.f;         // masked tail columns (poly gives 2^-125)
                 if (2 * i + 1 >= valid) x1 = 0.f;
               } else {
+#ifndef CQS_DBG_NO_EXP
                 x0 = ptx::ex2(x0);
                 x1 = ptx::ex2(x1);
+#endif
               }
               rs2[ii & 3] = ptx::fadd2(rs2[ii & 3], ptx::f2(x0, x1));
               pk[ii] = ptx::pack_bf16(x0, x1);
             }
-            ptx::tmem_st16(tS + c * 16, pk);
+            if (!kPstEnd) ptx::tmem_st16(tS + c * 16, pk);
+          }
+          if (kPstEnd) {   // one store pass after the last exponential (see kPstEnd)
+            ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pka[0]));
+            ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pka[32]));
           }
           if (kTrack) rmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
           const uint64_t rr = ptx::fadd2(ptx::fadd2(rs2[0], rs2[1]), ptx::fadd2(rs2[2], rs2[3]));
@@ -383,6 +413,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           // tile's max on the side; only when it exceeds m by more than the threshold (rare after
           // the first tiles) are O and l rescaled (O must hold PV_{j-1}) and the pass redone
           rowsum = exp_pass(m, std::true_type{}, rmax);
+          if (kPingPong<D> && two && !(t == 1 && j == n_kv - 1)) ptx::named_bar_arrive(2 - t, 256);
           const float mx = rmax * scale_log2;
           const bool need = mx > m + kRescaleThreshold;
           exact_pass = __any_sync(0xffffffffu, need);
@@ -407,12 +438,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           }
         }
         if (exact_pass) rowsum = exp_pass(m, std::false_type{}, rmax);
+        if (kPingPong<D> && two && j == 0 && !(t == 1 && j == n_kv - 1))
+          ptx::named_bar_arrive(2 - t, 256);
         l += rowsum;
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[t]);
-        if (kPingPong<D> && two && !(t == 1 && j == n_kv - 1)) ptx::named_bar_arrive(2 - t, 256);
 #ifdef CQS_DBG_TIMING
         DBG1_T0(ts2);
         if (lane == 0) DBG1_ADD(0, ts1 - ts0), DBG1_ADD(1, ts2 - ts1), DBG1_ADD(2, 1);

@@ -37,6 +37,13 @@ constexpr int kStageBytes = 16384;             // K half (2 boxes of 64 rows) or
 constexpr int kStages = CQS_PAIR_STAGES;
 constexpr int kSmemBytes = 2 * kQBytes + kStages * kStageBytes + 1024 + 512;
 constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 384;
+// P stored to TMEM after the whole exp pass (two x32 stores) instead of one x16 store per
+// 32-column chunk: the chunked stores' source registers are re-used by the next chunk's packs,
+// so every chunk waits until its tcgen05.st has read them (WAR on the STTM operands).
+#ifndef CQS_PST_END
+#define CQS_PST_END 0
+#endif
+constexpr bool kPstEnd = CQS_PST_END != 0;
 constexpr float kRescaleThreshold = 8.0f;
 // setmaxnreg split of the 384 x 168 launch registers: 4 producer / MMA / allocator warps at LO,
 // 8 softmax warps at HI, with 128 (168 - LO) = 256 (HI - 168) (an unbalanced .inc blocks forever)
@@ -56,6 +63,13 @@ static_assert(128 * (168 - CQS_PAIR_REG_LO) == 256 * (CQS_PAIR_REG_HI - 168), "r
 // whole 4 KB Q slice per instruction, so the S halves exceed the 128 B/clk SMEM operand bandwidth.
 // Experiment only (-DCQS_SPLIT_S).
 constexpr bool kSplitS = false;
+// Softmax sequencing: the two tiles' exp passes alternate (named barriers 1 / 2, 8 warps each) so
+// each runs alone on the SM sub-partition's MUFU while the tensor core works on the other tile;
+// the S load (tcgen05.ld) stays outside the sequenced region.
+#ifndef CQS_PAIR_SEQ
+#define CQS_PAIR_SEQ 0
+#endif
+constexpr bool kSeq = CQS_PAIR_SEQ != 0;
 // column pairs (i mod 8) whose exp2 runs as an FMA-pipe polynomial instead of MUFU.EX2
 #ifdef CQS_DBG_POLY_MASK
 constexpr uint32_t kPolyMask = CQS_DBG_POLY_MASK;
@@ -65,7 +79,7 @@ constexpr uint32_t kPolyMask = 0x0;
 }  // namespace pair
 
 #ifdef CQS_DBG_TIMING   // timing experiment only: per-role cycle accounting (tools/timing_probe.py)
-__device__ unsigned long long g_cqs_dbg[16];
+__device__ unsigned long long g_cqs_dbg[32];
 #define DBG_T0(v) const long long v = clock64()
 #define DBG_ADD(i, x) atomicAdd(&g_cqs_dbg[i], (unsigned long long)(x))
 #else
@@ -96,6 +110,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_loaded + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef CQS_DBG_TIMING
+  const long long k_c0 = clock64();
+  unsigned long long k_g0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(k_g0));
+#endif
   const uint32_t rank = ptx::cluster_ctarank();
   const bool leader = rank == 0;
 
@@ -151,6 +170,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
       int it = 0;
       auto stage_wait = [&](int s) {
         ptx::mbar_wait(&kv_empty[s], ((it / kStages) & 1) ^ 1);
+#ifdef CQS_DBG_NO_REFILL   // diagnostic only (wrong results): stages loaded once, then reused
+        if (it >= kStages) {
+          if (leader) ptx::mbar_arrive(&kv_full[s]);
+          return false;
+        }
+#endif
         if (leader) ptx::mbar_arrive_expect_tx(&kv_full[s], 2 * kStageBytes);
         return true;
       };
@@ -299,6 +324,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
 #endif
       KvCursor cur;
       cur.init(&tp, kmask, kv0);
+#ifdef CQS_DBG_TIMING
+      const long long tl0 = clock64();
+#endif
       for (int j = 0; j < n_kv; ++j) {
         const int valid = cur.valid();
         cur.next();
@@ -308,6 +336,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         DBG_T0(ts1);
 #ifdef CQS_DBG_TIMING
         dc[0] += ts1 - ts0, dc[2] += 1;
+#endif
+#ifdef CQS_DBG_NO_SMX   // diagnostic only (wrong results): no softmax work, only the barrier chain
+        m = 0.f, l = 1.f;
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_leader(&p_full[t]);
+        continue;
 #endif
         uint32_t sr[kBN];
         // registers in key order: with split S, keys [32c, 32c + 32) sit at column
@@ -329,6 +364,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
           for (int c = 0; c < kBN; ++c)
             if (c >= valid) s[c] = -INFINITY;
         }
+        // sequenced exp phases: tile t waits for the other tile's pass of this (t = 1) or the
+        // previous (t = 0) step; the first pass of tile 0 goes first
+        if (kSeq && two && !(t == 0 && j == 0)) ptx::named_bar_sync(1 + t, 256);
         // One exp2 pass: p = 2^(s*scale_log2 - m_use) fused per 32-column chunk with the packed
         // row sum, the bf16 pack and the tcgen05.st of P (sums / packs / stores fill the issue
         // slots between MUFU ops).  With TRACK it also takes the row max of the raw scores on the
@@ -342,9 +380,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) mx4[u] = -INFINITY;
           }
+          uint32_t pka[kBN / 2];   // packed bf16 P of the whole row
 #pragma unroll
           for (int c = 0; c < kBN / 32; ++c) {
-            uint32_t pk[16];
+            uint32_t(&pk)[16] = *reinterpret_cast<uint32_t(*)[16]>(&pka[16 * c]);
 #pragma unroll
             for (int ii = 0; ii < 16; ++ii) {
               const int i = 16 * c + ii;
@@ -353,19 +392,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
                                           fmaxf(fmaxf(s[2 * i], s[2 * i + 1]),
                                                 fmaxf(s[2 * i + 2], s[2 * i + 3])));
               float x0, x1;
+#ifdef CQS_DBG_NO_EXP   // diagnostic only (wrong results): P = raw S, no exponentials
+              x0 = s[2 * i], x1 = s[2 * i + 1];
+              if (false) {
+#else
               ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
               if ((kPolyMask >> (i & 7)) & 1) {
+#endif
                 ptx::exp2_poly_pair(x0, x1);
                 if (2 * i >= valid) x0 = 0.f;   // masked tail columns (poly gives 2^-125)
                 if (2 * i + 1 >= valid) x1 = 0.f;
               } else {
+#ifndef CQS_DBG_NO_EXP
                 x0 = ptx::ex2(x0);
                 x1 = ptx::ex2(x1);
+#endif
               }
               rs2[ii & 3] = ptx::fadd2(rs2[ii & 3], ptx::f2(x0, x1));
               pk[ii] = ptx::pack_bf16(x0, x1);
             }
-            ptx::tmem_st16(tS + c * 16, pk);
+            if (!kPstEnd) ptx::tmem_st16(tS + c * 16, pk);
+          }
+          if (kPstEnd) {   // one store pass after the last exponential (see kPstEnd)
+            ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pka[0]));
+            ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pka[32]));
           }
           if (kTrack) rmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
           const uint64_t rr = ptx::fadd2(ptx::fadd2(rs2[0], rs2[1]), ptx::fadd2(rs2[2], rs2[3]));
@@ -375,7 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         };
         float rowsum = 0.f, rmax = 0.f;
 #ifdef CQS_DBG_TIMING
-        long long tp_max = 0, tp_gate = 0, tp_exp = 0;
+        long long tp_max = tp_ld, tp_gate = 0, tp_exp = 0;
 #define DBG_MARK(v) v = clock64()
 #else
 #define DBG_MARK(v)
@@ -401,6 +451,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
           // (2^8; rare after the first tiles) are O and l rescaled and the pass redone.
           DBG_MARK(tp_max);
           rowsum = exp_pass(m, std::true_type{}, rmax);
+          if (kSeq && two && !(t == 1 && j == n_kv - 1)) ptx::named_bar_arrive(2 - t, 256);
           const float mx = rmax * scale_log2;
           const bool need = mx > m + kRescaleThreshold;
           exact_pass = __any_sync(0xffffffffu, need);
@@ -426,6 +477,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         }
         DBG_MARK(tp_gate);
         if (exact_pass) rowsum = exp_pass(m, std::false_type{}, rmax);
+        if (kSeq && two && j == 0 && !(t == 1 && j == n_kv - 1)) ptx::named_bar_arrive(2 - t, 256);
         DBG_MARK(tp_exp);
         l += rowsum;
         ptx::tmem_st_wait();
@@ -446,6 +498,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
           if (i < 3 || i >= 7) DBG_ADD(i, dc[i]);
 #endif
       // ---- epilogue ----
+      DBG_T0(te0);
+#ifdef CQS_DBG_TIMING
+      if (lane == 0 && warp == 4) DBG_ADD(16, tl0 - k_c0), DBG_ADD(17, te0 - tl0), DBG_ADD(19, 1);
+#endif
       ptx::mbar_wait(&o_bar[t], (n_kv - 1) & 1);
       ptx::tc_fence_after();
       const int row_in_seg = q_off + t * 2 * kBM + int(rank) * kBM + r;
@@ -468,6 +524,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         }
       }
       if (live) acc_lse[idx] = w.lse;
+#ifdef CQS_DBG_TIMING
+      if (lane == 0) DBG_ADD(3, clock64() - te0);
+      if (lane == 0 && warp == 4) DBG_ADD(18, clock64() - k_c0);
+#endif
     }
   }
 
@@ -477,6 +537,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc_2sm(tmem, 512);
   }
+#ifdef CQS_DBG_TIMING
+  if (threadIdx.x == 0) {   // per-CTA lifetime: cycles, ns (-> in-kernel clock, SM occupancy)
+    unsigned long long k_g1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(k_g1));
+    DBG_ADD(12, clock64() - k_c0), DBG_ADD(13, k_g1 - k_g0), DBG_ADD(14, 1);
+  }
+#endif
 }
 
 #ifdef CQS_DBG_TIMING
@@ -484,7 +551,7 @@ extern "C" int cqs_dbg_read(unsigned long long* out, int n) {
   return int(cudaMemcpyFromSymbol(out, g_cqs_dbg, sizeof(unsigned long long) * n));
 }
 extern "C" int cqs_dbg_reset() {
-  unsigned long long z[16] = {};
+  unsigned long long z[32] = {};
   return int(cudaMemcpyToSymbol(g_cqs_dbg, z, sizeof(z)));
 }
 #endif
