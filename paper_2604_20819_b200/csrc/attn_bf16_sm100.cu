@@ -39,13 +39,16 @@ __device__ unsigned long long g_cqs_dbg1[16];
 #define DBG1_T0(v)
 #define DBG1_ADD(i, x) ((void)0)
 #endif
-// P stored to TMEM after the whole exp pass (two x32 stores) instead of one x16 store per
-// 32-column chunk: the chunked stores' source registers are re-used by the next chunk's packs,
-// so every chunk waits until its tcgen05.st has read them (WAR on the STTM operands).
-#ifndef CQS_PST_END
-#define CQS_PST_END 0
+// Rescale guard of the speculative pass: with kSumGuard the pass tracks no row max at all (the
+// FMNMX chains cost ~11% of the pass); a row is rescaled (exact max, O and l scaled, pass redone)
+// only when its P row sum against the running max exceeds kSumLimit, i.e. some p = 2^(x - m) is
+// large.  Any reference max is exact (O / l and lse = m + log2 l are invariant under it); the guard
+// only keeps p, l and O far from fp32 overflow (l grows at most by kSumLimit per KV tile).
+#ifndef CQS_SUM_GUARD
+#define CQS_SUM_GUARD 1
 #endif
-constexpr bool kPstEnd = CQS_PST_END != 0;
+constexpr bool kSumGuard = CQS_SUM_GUARD != 0;
+constexpr float kSumLimit = 65536.0f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units (factor 256)
 // setmaxnreg split (see the register note in the kernel): 4 warps at LO, 8 softmax warps at HI
 // (56 / 224: no spills; measured +3.9% over 72 / 216 at D = 64: 725 vs 697 TFLOP/s, 3 runs each)
@@ -298,6 +301,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const uint32_t tS = tmem + lane_base + (t ? C::kColS1 : C::kColS0);
       const uint32_t tO = tmem + lane_base + (t ? C::kColO1 : C::kColO0);
       float m = -INFINITY, l = 0.f;
+      const uint32_t a_sfull = ptx::smem_u32(&s_full[t]), a_pfull = ptx::smem_u32(&p_full[t]);
       if constexpr (C::kQInTmem) {
         // this thread's Q row (SW128 TMA box: 16-byte chunk c of row r sits at chunk c ^ (r & 7))
         // -> 32 packed bf16 pairs -> TMEM columns kColQ_t (same packing as P)
@@ -321,7 +325,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const int valid = cur.valid();
         cur.next();
         DBG1_T0(ts0);
-        ptx::mbar_wait(&s_full[t], j & 1);
+        ptx::mbar_wait_a(a_sfull, j & 1);
         ptx::tc_fence_after();
         DBG1_T0(ts1);
         uint32_t sr[kBN];
@@ -349,10 +353,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) mx4[u] = -INFINITY;
           }
-          uint32_t pka[kBN / 2];   // packed bf16 P of the whole row
 #pragma unroll
           for (int c = 0; c < kBN / 32; ++c) {
-            uint32_t(&pk)[16] = *reinterpret_cast<uint32_t(*)[16]>(&pka[16 * c]);
+            uint32_t pk[16];
 #pragma unroll
             for (int ii = 0; ii < 16; ++ii) {
               const int i = 16 * c + ii;
@@ -380,11 +383,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
               rs2[ii & 3] = ptx::fadd2(rs2[ii & 3], ptx::f2(x0, x1));
               pk[ii] = ptx::pack_bf16(x0, x1);
             }
-            if (!kPstEnd) ptx::tmem_st16(tS + c * 16, pk);
-          }
-          if (kPstEnd) {   // one store pass after the last exponential (see kPstEnd)
-            ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pka[0]));
-            ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pka[32]));
+            ptx::tmem_st16(tS + c * 16, pk);
           }
           if (kTrack) rmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
           const uint64_t rr = ptx::fadd2(ptx::fadd2(rs2[0], rs2[1]), ptx::fadd2(rs2[2], rs2[3]));
@@ -394,8 +393,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         };
         float rowsum = 0.f, rmax = 0.f;
         bool exact_pass = true;
-        if (j == 0) {
-          // first tile: exact row max first (8 FMNMX3 chains, then a small tree)
+        auto row_max = [&]() {   // exact raw row max of the tile (8 FMNMX3 chains, then a tree)
           float mx8[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) mx8[u] = s[u];
@@ -406,21 +404,35 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], s[kBN - 8 + u]);   // last 8 columns
-          m = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                    fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
+          return fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        };
+        if (j == 0) {
+          m = row_max() * scale_log2;   // first tile: exact row max first
         } else {
           // speculative max: exponentiate against the running max right away and take this
           // tile's max on the side; only when it exceeds m by more than the threshold (rare after
           // the first tiles) are O and l rescaled (O must hold PV_{j-1}) and the pass redone
-          rowsum = exp_pass(m, std::true_type{}, rmax);
-          if (kPingPong<D> && two && !(t == 1 && j == n_kv - 1)) ptx::named_bar_arrive(2 - t, 256);
-          const float mx = rmax * scale_log2;
-          const bool need = mx > m + kRescaleThreshold;
+          rowsum = exp_pass(m, std::bool_constant<!kSumGuard>{}, rmax);
+          bool need;
+          float mx = 0.f;
+          if (kSumGuard) {
+            need = !(rowsum <= kSumLimit);   // some p > kSumLimit / kBN (also inf)
+          } else {
+            mx = rmax * scale_log2;
+            need = mx > m + kRescaleThreshold;
+          }
           exact_pass = __any_sync(0xffffffffu, need);
           if (exact_pass) {
-            const float m_new = need ? mx : m;
+            if (kSumGuard) {   // rare path: one FMNMX chain (few live registers)
+              mx = s[0];
+#pragma unroll
+              for (int c = 1; c < kBN; ++c) mx = fmaxf(mx, s[c]);
+              mx *= scale_log2;
+            }
+            const float m_new = need ? fmaxf(m, mx) : m;
             ptx::tmem_st_wait();
-            ptx::mbar_wait(&o_bar[t], (j - 1) & 1);
+            ptx::mbar_wait(&o_bar[t], (j - 1) & 1);   // O must hold PV_{j-1}
             ptx::tc_fence_after();
             const float f = need ? ptx::ex2(m - m_new) : 1.f;
 #pragma unroll
@@ -444,7 +456,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+        if (lane == 0) ptx::mbar_arrive_a(a_pfull);
 #ifdef CQS_DBG_TIMING
         DBG1_T0(ts2);
         if (lane == 0) DBG1_ADD(0, ts1 - ts0), DBG1_ADD(1, ts2 - ts1), DBG1_ADD(2, 1);

@@ -37,13 +37,16 @@ constexpr int kStageBytes = 16384;             // K half (2 boxes of 64 rows) or
 constexpr int kStages = CQS_PAIR_STAGES;
 constexpr int kSmemBytes = 2 * kQBytes + kStages * kStageBytes + 1024 + 512;
 constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 384;
-// P stored to TMEM after the whole exp pass (two x32 stores) instead of one x16 store per
-// 32-column chunk: the chunked stores' source registers are re-used by the next chunk's packs,
-// so every chunk waits until its tcgen05.st has read them (WAR on the STTM operands).
-#ifndef CQS_PST_END
-#define CQS_PST_END 0
+// Rescale guard of the speculative pass: with kSumGuard the pass tracks no row max at all (the
+// FMNMX chains cost ~11% of the pass); a row is rescaled (exact max, O and l scaled, pass redone)
+// only when its P row sum against the running max exceeds kSumLimit, i.e. some p = 2^(x - m) is
+// large.  Any reference max is exact (O / l and lse = m + log2 l are invariant under it); the guard
+// only keeps p, l and O far from fp32 overflow (l grows at most by kSumLimit per KV tile).
+#ifndef CQS_SUM_GUARD
+#define CQS_SUM_GUARD 1
 #endif
-constexpr bool kPstEnd = CQS_PST_END != 0;
+constexpr bool kSumGuard = CQS_SUM_GUARD != 0;
+constexpr float kSumLimit = 65536.0f;
 constexpr float kRescaleThreshold = 8.0f;
 // setmaxnreg split of the 384 x 168 launch registers: 4 producer / MMA / allocator warps at LO,
 // 8 softmax warps at HI, with 128 (168 - LO) = 256 (HI - 168) (an unbalanced .inc blocks forever)
@@ -63,13 +66,9 @@ static_assert(128 * (168 - CQS_PAIR_REG_LO) == 256 * (CQS_PAIR_REG_HI - 168), "r
 // whole 4 KB Q slice per instruction, so the S halves exceed the 128 B/clk SMEM operand bandwidth.
 // Experiment only (-DCQS_SPLIT_S).
 constexpr bool kSplitS = false;
-// Softmax sequencing: the two tiles' exp passes alternate (named barriers 1 / 2, 8 warps each) so
-// each runs alone on the SM sub-partition's MUFU while the tensor core works on the other tile;
-// the S load (tcgen05.ld) stays outside the sequenced region.
-#ifndef CQS_PAIR_SEQ
-#define CQS_PAIR_SEQ 0
-#endif
-constexpr bool kSeq = CQS_PAIR_SEQ != 0;
+// (Measured and dropped in round 2, all neutral or slower on C2 — profiles/r02_notes.md:
+// alternating the two tiles' exp passes with named barriers, storing P after the whole pass,
+// releasing P to the MMA in two parts with a deferred rescale.)
 // column pairs (i mod 8) whose exp2 runs as an FMA-pipe polynomial instead of MUFU.EX2
 #ifdef CQS_DBG_POLY_MASK
 constexpr uint32_t kPolyMask = CQS_DBG_POLY_MASK;
@@ -319,6 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
       const uint32_t tS = tmem + lane_base + (t ? kColS1 : kColS0);
       const uint32_t tO = tmem + lane_base + (t ? kColO1 : kColO0);
       float m = -INFINITY, l = 0.f;
+      const uint32_t a_sfull = ptx::smem_u32(&s_full[t]), a_pfull = ptx::smem_u32(&p_full[t]);
 #ifdef CQS_DBG_TIMING
       long long dc[12] = {};
 #endif
@@ -331,7 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         const int valid = cur.valid();
         cur.next();
         DBG_T0(ts0);
-        ptx::mbar_wait(&s_full[t], j & 1);
+        ptx::mbar_wait_a(a_sfull, j & 1);
         ptx::tc_fence_after();
         DBG_T0(ts1);
 #ifdef CQS_DBG_TIMING
@@ -341,7 +341,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         m = 0.f, l = 1.f;
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_leader(&p_full[t]);
+        if (lane == 0) ptx::mbar_arrive_leader_a(a_pfull);
         continue;
 #endif
         uint32_t sr[kBN];
@@ -364,9 +364,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
           for (int c = 0; c < kBN; ++c)
             if (c >= valid) s[c] = -INFINITY;
         }
-        // sequenced exp phases: tile t waits for the other tile's pass of this (t = 1) or the
-        // previous (t = 0) step; the first pass of tile 0 goes first
-        if (kSeq && two && !(t == 0 && j == 0)) ptx::named_bar_sync(1 + t, 256);
         // One exp2 pass: p = 2^(s*scale_log2 - m_use) fused per 32-column chunk with the packed
         // row sum, the bf16 pack and the tcgen05.st of P (sums / packs / stores fill the issue
         // slots between MUFU ops).  With TRACK it also takes the row max of the raw scores on the
@@ -380,10 +377,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) mx4[u] = -INFINITY;
           }
-          uint32_t pka[kBN / 2];   // packed bf16 P of the whole row
 #pragma unroll
           for (int c = 0; c < kBN / 32; ++c) {
-            uint32_t(&pk)[16] = *reinterpret_cast<uint32_t(*)[16]>(&pka[16 * c]);
+            uint32_t pk[16];
 #pragma unroll
             for (int ii = 0; ii < 16; ++ii) {
               const int i = 16 * c + ii;
@@ -411,11 +407,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
               rs2[ii & 3] = ptx::fadd2(rs2[ii & 3], ptx::f2(x0, x1));
               pk[ii] = ptx::pack_bf16(x0, x1);
             }
-            if (!kPstEnd) ptx::tmem_st16(tS + c * 16, pk);
-          }
-          if (kPstEnd) {   // one store pass after the last exponential (see kPstEnd)
-            ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pka[0]));
-            ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pka[32]));
+            ptx::tmem_st16(tS + c * 16, pk);
           }
           if (kTrack) rmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
           const uint64_t rr = ptx::fadd2(ptx::fadd2(rs2[0], rs2[1]), ptx::fadd2(rs2[2], rs2[3]));
@@ -431,8 +423,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
 #define DBG_MARK(v)
 #endif
         bool exact_pass = true;   // run the plain pass against the final m
-        if (j == 0) {
-          // first tile: exact row max first (8 FMNMX3 chains, then a small tree)
+        auto row_max = [&]() {   // exact raw row max of the tile (8 FMNMX3 chains, then a tree)
           float mx8[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) mx8[u] = s[u];
@@ -443,20 +434,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
           }
 #pragma unroll
           for (int u = 0; u < 8; ++u) mx8[u] = fmaxf(mx8[u], s[kBN - 8 + u]);   // last 8 columns
-          m = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                    fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
+          return fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        };
+        if (j == 0) {
+          m = row_max() * scale_log2;   // first tile: exact row max first
         } else {
           // speculative max: exponentiate against the running max m right away and take this
           // tile's max on the side; only if it exceeds m by more than the rescale threshold
           // (2^8; rare after the first tiles) are O and l rescaled and the pass redone.
           DBG_MARK(tp_max);
-          rowsum = exp_pass(m, std::true_type{}, rmax);
-          if (kSeq && two && !(t == 1 && j == n_kv - 1)) ptx::named_bar_arrive(2 - t, 256);
-          const float mx = rmax * scale_log2;
-          const bool need = mx > m + kRescaleThreshold;
+          rowsum = exp_pass(m, std::bool_constant<!kSumGuard>{}, rmax);
+          bool need;
+          float mx = 0.f;
+          if (kSumGuard) {
+            need = !(rowsum <= kSumLimit);   // some p > kSumLimit / kBN (also inf)
+          } else {
+            mx = rmax * scale_log2;
+            need = mx > m + kRescaleThreshold;
+          }
           exact_pass = __any_sync(0xffffffffu, need);
           if (exact_pass) {
-            const float m_new = need ? mx : m;
+            if (kSumGuard) {   // rare path: one FMNMX chain (few live registers)
+              mx = s[0];
+#pragma unroll
+              for (int c = 1; c < kBN; ++c) mx = fmaxf(mx, s[c]);
+              mx *= scale_log2;
+            }
+            const float m_new = need ? fmaxf(m, mx) : m;
             ptx::tmem_st_wait();
             ptx::mbar_wait(&o_bar[t], (j - 1) & 1);   // O must hold PV_{j-1}
             ptx::tc_fence_after();
@@ -477,13 +482,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         }
         DBG_MARK(tp_gate);
         if (exact_pass) rowsum = exp_pass(m, std::false_type{}, rmax);
-        if (kSeq && two && j == 0 && !(t == 1 && j == n_kv - 1)) ptx::named_bar_arrive(2 - t, 256);
         DBG_MARK(tp_exp);
         l += rowsum;
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_leader(&p_full[t]);
+        if (lane == 0) ptx::mbar_arrive_leader_a(a_pfull);
 #ifdef CQS_DBG_TIMING
         {
           const long long tp_end = clock64();
