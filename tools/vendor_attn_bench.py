@@ -27,6 +27,70 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def time_calls(fn, args):
+    import torch
+    from bench import ClockSampler
+    for _ in range(args.warmup):
+        fn()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as cs:
+        e0.record(st)
+        for _ in range(args.steps):
+            fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / args.steps, cs.summary()
+
+
+def bwd_run(be, D, q, k, v, do, o_c, lse_c, flops, args):
+    """Backward time of one backend: ours directly; library ones as (fwd + bwd) - fwd."""
+    import torch
+    import torch.nn.functional as F
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    import paper_2604_20819_b200 as cqs
+    row = {"backend": be, "D": D, "pass": "backward"}
+    try:
+        if be == "cqs":
+            ms, clk = time_calls(lambda: cqs.attention_backward(q, k, v, o_c, do, lse_c, depth=1), args)
+        else:
+            if be == "cudnn":
+                ctx = lambda: sdpa_kernel(SDPBackend.CUDNN_ATTENTION)
+                f = lambda a, b, c: F.scaled_dot_product_attention(a, b, c)
+            elif be == "torch_fa":
+                ctx = lambda: sdpa_kernel(SDPBackend.FLASH_ATTENTION)
+                f = lambda a, b, c: F.scaled_dot_product_attention(a, b, c)
+            elif be == "flash_attn":
+                from flash_attn import flash_attn_func
+                import contextlib
+                ctx = contextlib.nullcontext
+                f = lambda a, b, c: flash_attn_func(a.transpose(1, 2), b.transpose(1, 2),
+                                                    c.transpose(1, 2)).transpose(1, 2)
+            else:
+                raise ValueError(be)
+            qg, kg, vg = (t.detach().clone().requires_grad_(True) for t in (q, k, v))
+
+            def fb():
+                with ctx():
+                    o = f(qg, kg, vg)
+                o.backward(do)
+                qg.grad = kg.grad = vg.grad = None
+
+            def fo():
+                with ctx(), torch.no_grad():
+                    f(qg, kg, vg)
+            ms_fb, clk = time_calls(fb, args)
+            ms_f, _ = time_calls(fo, args)
+            ms = ms_fb - ms_f
+            row["ms_fwd_plus_bwd"] = ms_fb
+        row.update(ms=ms, tflops=flops / (ms * 1e-3) / 1e12, clocks=clk)
+    except Exception as ex:
+        row["error"] = ("%s: %s" % (type(ex).__name__, ex)).splitlines()[0][:300]
+    torch.cuda.empty_cache()
+    return row
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--D", type=int, nargs="+", default=[128, 64])
@@ -35,6 +99,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--backends", nargs="+", default=["cqs", "cudnn", "torch_fa", "flash_attn"])
+    ap.add_argument("--bwd", action="store_true",
+                    help="time the backward instead (10 N^2 D H algorithmic FLOPs): ours = "
+                         "cqs.attention_backward, cuDNN / FA = autograd of SDPA (fwd+bwd minus fwd)")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
 
@@ -53,9 +120,16 @@ def main():
     for D in args.D:
         q, k, v = cqs_synth.torch_qkv(1, args.H, args.N, D, 20260418, dtype=torch.bfloat16,
                                       device=dev)
-        flops = 4.0 * args.N * args.N * D * args.H
+        flops = (10.0 if args.bwd else 4.0) * args.N * args.N * D * args.H
         ref_out = None
+        if args.bwd:
+            do = cqs_synth.torch_tensor((1, args.H, args.N, D), 20260418, "do", torch.bfloat16, dev)
+            o_c, lse_c = cqs.attention(q, k, v, depth=1)
         for be in args.backends:
+            if args.bwd:
+                res["runs"].append(bwd_run(be, D, q, k, v, do, o_c, lse_c, flops, args))
+                print(json.dumps(res["runs"][-1]), flush=True)
+                continue
             row = {"backend": be, "D": D}
             try:
                 if be == "cqs":
