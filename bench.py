@@ -626,7 +626,7 @@ def main():
         dist.destroy_process_group()
         return 0
     peaks, peak_src = load_peaks()
-    kname = "attn_bf16_sm100_2cta_kernel" if D == 128 else "attn_bf16_sm100_kernel<%d>" % D
+    kname = "attn_bf16_sm100_2cta_kernel" if D == 128 else "attn_bf16_sm100_3t_kernel"
     traffic = ncu_traffic(kname)
     # the peak that matches the timing (task rules): the attention kernels run back to back for the
     # whole timed region (>= 1 s, under sw_power_cap), so the SUSTAINED measured bf16 peak; the

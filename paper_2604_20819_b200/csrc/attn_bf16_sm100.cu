@@ -512,24 +512,37 @@ static cudaError_t launch_bf16_impl(const CUtensorMap* maps, const TaskParams& t
 
 cudaError_t launch_attn_bf16_pair(const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
                                   float* acc_lse, float scale, cudaStream_t stream);
+cudaError_t launch_attn_bf16_3t(const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
+                                float* acc_lse, float scale, cudaStream_t stream);
 
 // D = 128 runs on CTA pairs (cta_group::2, 512 query rows per item; K maps with 64-row boxes);
 // D = 64 on the two-tile kernel above (a double-buffered-S alternative measured 680 vs 695
 // TFLOP/s on C2-d64; kept out of the build in tools/experiments/attn_bf16_sm100_d64.cu).
 // Callers size work items with attn_rows_per_item and build the Q / K / V maps with
 // attn_box_rows(D, 0 / 1 / 2).
+// D = 64 runs on the three-tile kernel (attn_bf16_sm100_3t.cu: 384 query rows per CTA, 96-key
+// K/V tiles) unless built with -DCQS_D64_3T=0 (the two-tile kernel above, 256 rows, 128 keys).
+#ifndef CQS_D64_3T
+#define CQS_D64_3T 1
+#endif
+#ifndef CQS_T3_TILES
+#define CQS_T3_TILES 3
+#define CQS_T3_BN 96
+#endif
 int attn_rows_per_item(int D) {
   if (D == 128) return 512;
-  return 256;
+  return CQS_D64_3T ? 128 * CQS_T3_TILES : 256;
 }
 int attn_box_rows(int D, int which) {
   if (D == 128 && which == 1) return 64;
+  if (D == 64 && CQS_D64_3T && which != 0) return CQS_T3_BN;
   return 128;
 }
 
 cudaError_t launch_attn_bf16(int D, const CUtensorMap* maps, const TaskParams& tp, float* acc_o,
                              float* acc_lse, float scale, cudaStream_t stream) {
   if (D == 128) return launch_attn_bf16_pair(maps, tp, acc_o, acc_lse, scale, stream);
+  if (D == 64 && CQS_D64_3T) return launch_attn_bf16_3t(maps, tp, acc_o, acc_lse, scale, stream);
   if (D == 64) return launch_bf16_impl<64>(maps, tp, acc_o, acc_lse, scale, stream);
   return cudaErrorInvalidValue;
 }

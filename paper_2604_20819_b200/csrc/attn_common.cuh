@@ -12,14 +12,15 @@ constexpr int kBN = 128;   // keys per KV tile
 // visit every tile once.  Work items start at different tiles (kv_start below) so the CTAs in
 // flight do not all request the same K/V lines from L2 at the same moment; the softmax is
 // order-independent (online max / LSE), only the fp32 rounding order changes.
-struct KvCursor {
+template <int BN = kBN>
+struct KvCursorT {
   uint32_t mask0, mask;
   int seg, kt, ntile;
   const TaskParams* tp;
   __device__ __forceinline__ void set_seg() {
     seg = mask ? __ffs(mask) - 1 : 0;
     kt = 0;
-    ntile = mask ? (tp->seg_len[seg] + kBN - 1) / kBN : 0;
+    ntile = mask ? (tp->seg_len[seg] + BN - 1) / BN : 0;
   }
   __device__ __forceinline__ void init(const TaskParams* p, uint32_t m, int start = 0) {
     tp = p;
@@ -32,8 +33,8 @@ struct KvCursor {
     }
     kt = start;
   }
-  __device__ __forceinline__ int row() const { return tp->seg_src[seg] + kt * kBN; }
-  __device__ __forceinline__ int valid() const { return min(kBN, tp->seg_len[seg] - kt * kBN); }
+  __device__ __forceinline__ int row() const { return tp->seg_src[seg] + kt * BN; }
+  __device__ __forceinline__ int valid() const { return min(BN, tp->seg_len[seg] - kt * BN); }
   __device__ __forceinline__ void next() {
     if (++kt == ntile) {
       mask &= mask - 1;
@@ -42,6 +43,7 @@ struct KvCursor {
     }
   }
 };
+using KvCursor = KvCursorT<kBN>;
 
 // First KV tile of work item `item` (of n_kv tiles).  CQS_KV_STAGGER = tile stride between
 // consecutive items (0: every item starts at tile 0).
