@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -257,6 +258,9 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
   // flush buffers instead of being written back to the host accumulator and re-read by a final
   // pass.  fin_g[g] = the row ranges whose last subtree is g (same sweep as fin, over the nodes).
   std::vector<std::vector<std::pair<int64_t, int64_t>>> fin_g;
+  // first_g[g] = the row ranges whose FIRST subtree is g: the host accumulator holds nothing for
+  // them yet, so their flush is a plain copy of the device rows (no host upload, no merge)
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> first_g;
   bool direct_final = false;
   if (j > 0 && nmy > 0) {
     std::vector<std::pair<int64_t, int64_t>> ev;
@@ -277,8 +281,9 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       g0 = g1;
     }
     std::sort(ev.begin(), ev.end());
-    std::vector<int64_t> open_cnt(size_t(ng) + 1, 0), heap;
+    std::vector<int64_t> open_cnt(size_t(ng) + 1, 0), heap, heap_min;
     fin_g.assign(size_t(ng), {});
+    first_g.assign(size_t(ng), {});
     direct_final = true;
     int64_t row = 0;
     size_t e = 0;
@@ -289,6 +294,8 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
           if (open_cnt[size_t(t)]++ == 0) {
             heap.push_back(t);
             std::push_heap(heap.begin(), heap.end());
+            heap_min.push_back(t);
+            std::push_heap(heap_min.begin(), heap_min.end(), std::greater<int64_t>());
           }
         } else {
           --open_cnt[size_t(-t)];
@@ -298,6 +305,10 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
       while (!heap.empty() && open_cnt[size_t(heap.front())] == 0) {
         std::pop_heap(heap.begin(), heap.end());
         heap.pop_back();
+      }
+      while (!heap_min.empty() && open_cnt[size_t(heap_min.front())] == 0) {
+        std::pop_heap(heap_min.begin(), heap_min.end(), std::greater<int64_t>());
+        heap_min.pop_back();
       }
       const int64_t next = e < ev.size() ? std::min<int64_t>(ev[e].first, N) : N;
       if (heap.empty()) {
@@ -310,6 +321,11 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
           v.back().second += next - row;
         else
           v.push_back({row, next - row});
+        auto& w = first_g[size_t(heap_min.front() - 1)];
+        if (!w.empty() && w.back().first + w.back().second == row)
+          w.back().second += next - row;
+        else
+          w.push_back({row, next - row});
       }
       row = next;
     }
@@ -518,26 +534,52 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
     if (j > 0 && flushed_once) CK(cudaStreamWaitEvent(sc.fh, flush_done, 0));  // host rows settled
     const std::vector<std::pair<int64_t, int64_t>>* fg =
         direct_final ? &fin_g[size_t(gidx)] : nullptr;
+    const std::vector<std::pair<int64_t, int64_t>>* ff =
+        direct_final ? &first_g[size_t(gidx)] : nullptr;
+    // is `grow` inside one of the sorted disjoint intervals iv? cuts n at the next boundary
+    auto in_ranges = [](const std::vector<std::pair<int64_t, int64_t>>* iv, int64_t grow,
+                        int64_t& n) {
+      // node segments come in the node's chunk order (I order), not in row order: look up the
+      // first interval that ends after `grow`
+      size_t k = size_t(std::upper_bound(iv->begin(), iv->end(), grow,
+                                         [](int64_t r, const std::pair<int64_t, int64_t>& x) {
+                                           return r < x.first + x.second;
+                                         }) - iv->begin());
+      if (k < iv->size() && (*iv)[k].first <= grow) {
+        n = std::min(n, (*iv)[k].first + (*iv)[k].second - grow);
+        return true;
+      }
+      if (k < iv->size()) n = std::min(n, (*iv)[k].first - grow);
+      return false;
+    };
     for (size_t s = 0; s < node.size() && j > 0; ++s) {   // (j = 0: emitted task by task above)
       for (int64_t c0 = 0; c0 < node[s].len;) {
         const int64_t grow = node[s].start + c0, lrow = node_off[s] + c0;
         int64_t n = std::min(F, node[s].len - c0);
-        bool final_rows = false;
-        if (fg) {   // cut the run at the next final / non-final boundary
-          // node segments come in the node's chunk order (I order), not in row order: look up
-          // the first fin_g interval that ends after `grow`
-          size_t fk = size_t(std::upper_bound(fg->begin(), fg->end(), grow,
-                                              [](int64_t r, const std::pair<int64_t, int64_t>& iv) {
-                                                return r < iv.first + iv.second;
-                                              }) - fg->begin());
-          if (fk < fg->size() && (*fg)[fk].first <= grow) {
-            final_rows = true;
-            n = std::min(n, (*fg)[fk].first + (*fg)[fk].second - grow);
-          } else if (fk < fg->size()) {
-            n = std::min(n, (*fg)[fk].first - grow);
-          }
-        }
+        const bool final_rows = fg && in_ranges(fg, grow, n);   // last subtree of these rows
+        const bool first_rows = ff && in_ranges(ff, grow, n);   // first subtree of these rows
         c0 += n;
+        const float* po = acc_o + lrow * BH * D;
+        const float* pl = acc_l + lrow * BH;
+        if (first_rows && final_rows) {   // only subtree of these rows: final straight from acc
+          cqs_status s2 = emit_final(fb_acquire(), po, pl, grow, n);
+          if (s2 != CQS_OK) return s2;
+          continue;
+        }
+        if (first_rows) {   // nothing in the host rows yet: copy the device rows out
+          const int b = fb_acquire();
+          CK(cudaMemcpyAsync(fb_o[b], po, size_t(n * BH * D * 4), cudaMemcpyDeviceToDevice, st));
+          CK(cudaMemcpyAsync(fb_l[b], pl, size_t(n * BH * 4), cudaMemcpyDeviceToDevice, st));
+          CK(cudaEventRecord(fb_merged[b], st));
+          CK(cudaStreamWaitEvent(sc.fd, fb_merged[b], 0));
+          CK(cudaMemcpyAsync(hacc_o + grow * BH * D, fb_o[b], size_t(n * BH * D * 4),
+                             cudaMemcpyDeviceToHost, sc.fd));
+          CK(cudaMemcpyAsync(hacc_l + grow * BH, fb_l[b], size_t(n * BH * 4),
+                             cudaMemcpyDeviceToHost, sc.fd));
+          CK(cudaEventRecord(fb_free[b], sc.fd));
+          d2h += uint64_t(n * BH * (D + 1) * 4);
+          continue;
+        }
         const int b = fb_acquire();
         CK(cudaMemcpyAsync(fb_o[b], hacc_o + grow * BH * D, size_t(n * BH * D * 4),
                            cudaMemcpyHostToDevice, sc.fh));
@@ -545,8 +587,6 @@ cqs_status forward_streamed(const cqs_plan_t* p, const void* q, const void* k, c
                            cudaMemcpyHostToDevice, sc.fh));
         CK(cudaEventRecord(fb_loaded[b], sc.fh));
         CK(cudaStreamWaitEvent(st, fb_loaded[b], 0));
-        const float* po = acc_o + lrow * BH * D;
-        const float* pl = acc_l + lrow * BH;
         h2d += uint64_t(n * BH * (D + 1) * 4);
         if (final_rows) {   // merge + convert into the other flush buffer, download O / lse
           cqs_status s2 = emit_final(fb_acquire(), fb_o[b], fb_l[b], grow, n, po, pl);

@@ -219,11 +219,25 @@ def test_bf16_mixed_level_interest_sets(levels, N, depth):
                                      (255, 1), (256, 1), (257, 1), (511, 0), (512, 0), (513, 0),
                                      (1025, 1), (343, 3)])
 def test_bf16_tile_boundaries(N, depth, D):
-    """Ragged sizes around the kernels' tile and work-item edges (128-row tiles; 256-row items at
+    """Ragged sizes around the kernels' tile and work-item edges (128-row tiles; 384-row items at
     D=64, 512-row CTA-pair items at D=128, where one CTA of the pair or one tile may hold no row
     of the segment), one to three heads, single-token chunks at depth 1/3."""
     H = 1 + N % 3
     q, k, v = gen(1, H, N, D, 900 + N + D, bf16=True)
+    out, lse = cqs.attention(q, k, v, depth=depth)
+    torch.cuda.synchronize()
+    check_bf16(out, lse, *ref_dense(q, k, v))
+
+
+@pytest.mark.parametrize("N,depth", [(95, 0), (96, 0), (97, 0), (191, 0), (192, 0), (193, 0),
+                                     (383, 0), (384, 0), (385, 0), (769, 0), (672, 1), (679, 1),
+                                     (2689, 1)])
+def test_bf16_d64_three_tile_edges(N, depth):
+    """D = 64 runs three 128-row tiles per CTA (384-row items) over 96-key K/V tiles: ragged sizes
+    around the 96-key tile edges (a key segment's last tile with 1 / 95 / 96 valid keys), the
+    384-row item edges (items holding 1, 2 or 3 tiles) and depth-1 chunks of 96 +- 1 rows."""
+    H = 1 + N % 3
+    q, k, v = gen(1, H, N, 64, 1900 + N, bf16=True)
     out, lse = cqs.attention(q, k, v, depth=depth)
     torch.cuda.synchronize()
     check_bf16(out, lse, *ref_dense(q, k, v))
