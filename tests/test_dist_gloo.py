@@ -110,6 +110,36 @@ def test_two_rank_exchange_reproduces_dense(N, depth, shard, qkv_loc, tmp_path):
     assert tot_work == N * N
 
 
+@pytest.mark.parametrize("world", [3, 4])
+@pytest.mark.parametrize("N,depth,shard,qkv_loc", [(1030, 2, "lpt", "device"),
+                                                   (2500, 3, "contiguous", "device"),
+                                                   (2401, 3, "contiguous", "host")])
+def test_multi_rank_exchange_reproduces_dense(world, N, depth, shard, qkv_loc, tmp_path):
+    """The same data plane at 3 and 4 ranks (ragged row shards at 3): every task on exactly one
+    rank, every row held by some rank, each owner's merged shard equals dense attention."""
+    import cqs_synth
+    from oracle import cqs_oracle as O
+    H, D = 2, 32
+    mp.start_processes(_worker, args=(world, _free_port(), N, H, D, depth, str(tmp_path), shard,
+                                      qkv_loc),
+                       nprocs=world, start_method="fork")
+    q, k, v = (cqs_synth.numpy_tensor((1, H, N, D), 77, n) for n in ("q", "k", "v"))
+    Od, ld = O.dense_attention(q, k, v)
+    Od = Od[0].transpose(1, 0, 2)
+    ld = ld[0].transpose(1, 0)
+    tot_work, covered = 0, 0
+    for r in range(world):
+        w, row0, rows, acc_rows = np.load(tmp_path / ("w%d.npy" % r))
+        assert row0 == covered
+        covered += rows
+        tot_work += w
+        Om = np.load(tmp_path / ("o%d.npy" % r))
+        lm = np.load(tmp_path / ("l%d.npy" % r))
+        assert np.abs(Om - Od[row0:row0 + rows]).max() < 1e-12
+        assert np.abs(lm - ld[row0:row0 + rows]).max() < 1e-12
+    assert covered == N and tot_work == N * N
+
+
 def _bwd_worker(rank, world, port, N, H, D, depth, outdir):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
