@@ -56,16 +56,12 @@ constexpr float kRescaleThreshold = 8.0f;
 #define CQS_PAIR_REG_HI 224
 #endif
 static_assert(128 * (168 - CQS_PAIR_REG_LO) == 256 * (CQS_PAIR_REG_HI - 168), "register split");
-// Split S: S_t(j+1) is issued as two N = 64 halves.  Half 0 (keys 0-31 of CTA 0's K rows and
-// 64-95 of CTA 1's) lands in columns [64, 128) of the tile's S region, which the softmax has
-// already read into registers (it signals s_loaded right after its tcgen05.ld), so it can run
-// while the softmax is still exponentiating S_t(j); half 1 (keys 32-63, 96-127) lands in
-// columns [0, 64) after PV_t(j) has consumed P_t(j) there.  The softmax's serial wait per tile
-// shrinks from PV + S (1024 tensor cycles) to PV + S/2 (768).  Measured slower (1006 vs 1120
-// TFLOP/s on C2, softmax wait-for-S 1808 vs 1207 cycles per tile): an N = 64 SS MMA still reads the
-// whole 4 KB Q slice per instruction, so the S halves exceed the 128 B/clk SMEM operand bandwidth.
-// Experiment only (-DCQS_SPLIT_S).
-constexpr bool kSplitS = false;
+// Any-order MMA service: the MMA warp serves the two tiles in the order their P becomes ready
+// (try_wait polling) instead of strictly tile 0 then tile 1.
+#ifndef CQS_PAIR_ANYORDER
+#define CQS_PAIR_ANYORDER 0
+#endif
+constexpr bool kAnyOrder = CQS_PAIR_ANYORDER != 0;
 // (Measured and dropped in round 2, all neutral or slower on C2 — profiles/r02_notes.md:
 // alternating the two tiles' exp passes with named barriers, storing P after the whole pass,
 // releasing P to the MMA in two parts with a deferred rescale.)
@@ -105,8 +101,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
   uint64_t* s_full = kv_empty + kStages;               // both: S_t ready (multicast commit)
   uint64_t* p_full = s_full + 2;                       // leader: 8 softmax warps of the pair
   uint64_t* o_bar = p_full + 2;                        // both: PV_t retired (multicast commit)
-  uint64_t* s_loaded = o_bar + 2;                      // leader: S_t read into registers (8 warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_loaded + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_bar + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef CQS_DBG_TIMING
@@ -142,7 +137,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
       ptx::mbar_init(&s_full[t], 1);
       ptx::mbar_init(&p_full[t], 8);
       ptx::mbar_init(&o_bar[t], 1);
-      ptx::mbar_init(&s_loaded[t], 8);
     }
     ptx::fence_barrier_init();
   }
@@ -224,21 +218,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         }
         ptx::mma_commit_2sm_elect(&s_full[t]);
       };
-      // one N = 64 half of S_t (see kSplitS): B = 32 key rows at row offset 32 h of each CTA's K
-      // half-tile; half 0 -> columns [64, 128), half 1 -> columns [0, 64) of the tile's S region
-      constexpr uint32_t idesc_qk_half = ptx::idesc_bf16(2 * kBM, kBN / 2, 0, 0);   // M=256, N=64
-      auto issue_S_half = [&](int t, int s, int h) {
-        const uint64_t qa = dq0 + uint64_t((t * kQBytes) >> 4);
-        const uint64_t kb = dkv0 + uint64_t((s * kStageBytes + h * 32 * 128) >> 4);
-        const uint32_t d = tmem + (t ? kColS1 : kColS0) + (h ? 0 : 64);
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t qo = ((ks >> 2) * (kBM * 128) + (ks & 3) * 32) >> 4;
-          const uint32_t ko = ((ks >> 2) * (kKHalfRows * 128) + (ks & 3) * 32) >> 4;
-          ptx::mma_ss_2sm_elect(d, qa + qo, kb + ko, idesc_qk_half, ks > 0);
-        }
-        if (h) ptx::mma_commit_2sm_elect(&s_full[t]);
-      };
       auto issue_PV = [&](int t, int s, bool acc) {
         const uint64_t vb = dv0 + uint64_t((s * kStageBytes) >> 4);
         const uint32_t d = tmem + (t ? kColO1 : kColO0), pa = tmem + (t ? kColS1 : kColS0);
@@ -258,14 +237,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
       ptx::mbar_wait(&kv_full[sK0], (it / kStages) & 1);
       ++it;
       ptx::tc_fence_after();
-      if (kSplitS) {
-        issue_S_half(0, sK0, 0);
-        issue_S_half(0, sK0, 1);
-        if (two) issue_S_half(1, sK0, 0), issue_S_half(1, sK0, 1);
-      } else {
-        issue_S(0, sK0);
-        if (two) issue_S(1, sK0);
-      }
+      issue_S(0, sK0);
+      if (two) issue_S(1, sK0);
       ptx::mma_commit_2sm_elect(&kv_empty[sK0]);
       for (int j = 0; j < n_kv; ++j) {
         int sKn = -1;
@@ -278,24 +251,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         ptx::mbar_wait(&kv_full[sV], (it / kStages) & 1);
         ++it;
         ptx::tc_fence_after();
-        for (int t = 0; t < (two ? 2 : 1); ++t) {
-          if (kSplitS && sKn >= 0) {   // S_t(j+1) half 0 as soon as the softmax has read S_t(j)
-            ptx::mbar_wait(&s_loaded[t], j & 1);
-            ptx::tc_fence_after();
-            issue_S_half(t, sKn, 0);
+        auto serve = [&](int t) {   // O_t += P_t V_j, then S_t(j+1) over the consumed P_t
+          ptx::tc_fence_after();
+          issue_PV(t, sV, j > 0);
+          if (sKn >= 0) issue_S(t, sKn);
+        };
+        int first = 0;   // with kAnyOrder: the tile whose P is ready first is served first
+        if (kAnyOrder && two)
+          for (;; ) {
+            if (ptx::mbar_try_wait(&p_full[0], j & 1)) break;
+            if (ptx::mbar_try_wait(&p_full[1], j & 1)) {
+              first = 1;
+              break;
+            }
           }
+        for (int k = 0; k < (two ? 2 : 1); ++k) {
+          const int t = k ? 1 - first : first;
           DBG_T0(tw0);
           ptx::mbar_wait(&p_full[t], j & 1);
 #ifdef CQS_DBG_TIMING
           DBG_T0(tw1);
           mma_pwait += tw1 - tw0;
 #endif
-          ptx::tc_fence_after();
-          issue_PV(t, sV, j > 0);
-          if (sKn >= 0) {
-            if (kSplitS) issue_S_half(t, sKn, 1);
-            else issue_S(t, sKn);
-          }
+          serve(t);
         }
         ptx::mma_commit_2sm_elect(&kv_empty[sV]);
         if (sKn >= 0) ptx::mma_commit_2sm_elect(&kv_empty[sKn]);
@@ -345,18 +323,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
         continue;
 #endif
         uint32_t sr[kBN];
-        // registers in key order: with split S, keys [32c, 32c + 32) sit at column
-        // {64, 0, 96, 32}[c] (half 0 holds keys 0-31 | 64-95, half 1 keys 32-63 | 96-127)
 #pragma unroll
         for (int c = 0; c < kBN / 32; ++c)
-          ptx::tmem_ld32(tS + (kSplitS ? ((c & 1) ? 0 : 64) + (c >> 1) * 32 : c * 32),
-                         *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+          ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
         ptx::tmem_ld_wait();
-        if (kSplitS) {   // S_t(j) is in registers: columns [64, 128) may take S_t(j+1) half 0
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive_leader(&s_loaded[t]);
-        }
         DBG_T0(tp_ld);
         float* s = reinterpret_cast<float*>(sr);
         if (valid < kBN) {

@@ -63,6 +63,10 @@ static_assert(128 * (kLaunchRegs - CQS_T3_REG_LO) == 128 * kTiles * (CQS_T3_REG_
 #define CQS_T3_POLY_MASK 0x0
 #endif
 constexpr uint32_t kPolyMask = CQS_T3_POLY_MASK;
+#ifndef CQS_T3_ANYORDER
+#define CQS_T3_ANYORDER 1
+#endif
+constexpr bool kAnyOrder = CQS_T3_ANYORDER != 0;
 }  // namespace t3
 
 __global__ void __launch_bounds__(t3::kThreads, 1)
@@ -196,11 +200,26 @@ __global__ void __launch_bounds__(t3::kThreads, 1)
         ptx::mbar_wait(&kv_full[sV], (it / kStages) & 1);
         ++it;
         ptx::tc_fence_after();
-        for (int t = 0; t < ntile; ++t) {
-          ptx::mbar_wait(&p_full[t], j & 1);
-          ptx::tc_fence_after();
-          issue_PV(t, sV, j > 0);
-          if (sKn >= 0) issue_S(t, sKn);
+        if (kAnyOrder) {
+          // serve the tiles in the order their P becomes ready (polling), not strictly 0, 1, 2
+          uint32_t pending = (1u << ntile) - 1;
+          while (pending) {
+#pragma unroll
+            for (int t = 0; t < kTiles; ++t) {
+              if (!((pending >> t) & 1) || !ptx::mbar_try_wait(&p_full[t], j & 1)) continue;
+              pending &= ~(1u << t);
+              ptx::tc_fence_after();
+              issue_PV(t, sV, j > 0);
+              if (sKn >= 0) issue_S(t, sKn);
+            }
+          }
+        } else {
+          for (int t = 0; t < ntile; ++t) {
+            ptx::mbar_wait(&p_full[t], j & 1);
+            ptx::tc_fence_after();
+            issue_PV(t, sV, j > 0);
+            if (sKn >= 0) issue_S(t, sKn);
+          }
         }
         ptx::mma_commit_elect(&kv_empty[sV]);
         if (sKn >= 0) ptx::mma_commit_elect(&kv_empty[sKn]);
