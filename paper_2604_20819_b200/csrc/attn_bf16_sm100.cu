@@ -180,13 +180,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const int s = it % C::kStages;
         const uint32_t ph = (it / C::kStages) & 1;
         ptx::mbar_wait(&kv_empty[s], ph ^ 1);
-#ifdef CQS_DBG_NO_REFILL   // diagnostic only (wrong results): stages loaded once, then reused
-        if (it >= C::kStages) {
-          ptx::mbar_arrive(&kv_full[s]);
-          ++it;
-          return;
-        }
-#endif
         ptx::mbar_arrive_expect_tx(&kv_full[s], C::kKVBytes);
         for (int bx = 0; bx < C::kBoxes; ++bx)
           ptx::tma_load_4d(sKV + s * C::kKVBytes + bx * kBN * 128, map, &kv_full[s], bx * 64, row,
@@ -364,21 +357,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                                           fmaxf(fmaxf(s[2 * i], s[2 * i + 1]),
                                                 fmaxf(s[2 * i + 2], s[2 * i + 3])));
               float x0, x1;
-#ifdef CQS_DBG_NO_EXP   // diagnostic only (wrong results): P = raw S, no exponentials
-              x0 = s[2 * i], x1 = s[2 * i + 1];
-              if (false) {
-#else
               ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
               if ((kPolyMask<D> >> (i & 7)) & 1) {
-#endif
                 ptx::exp2_poly_pair(x0, x1);
                 if (2 * i >= valid) x0 = 0.f;         // masked tail columns (poly gives 2^-125)
                 if (2 * i + 1 >= valid) x1 = 0.f;
               } else {
-#ifndef CQS_DBG_NO_EXP
                 x0 = ptx::ex2(x0);
                 x1 = ptx::ex2(x1);
-#endif
               }
               rs2[ii & 3] = ptx::fadd2(rs2[ii & 3], ptx::f2(x0, x1));
               pk[ii] = ptx::pack_bf16(x0, x1);

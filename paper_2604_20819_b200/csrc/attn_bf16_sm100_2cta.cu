@@ -163,12 +163,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
       int it = 0;
       auto stage_wait = [&](int s) {
         ptx::mbar_wait(&kv_empty[s], ((it / kStages) & 1) ^ 1);
-#ifdef CQS_DBG_NO_REFILL   // diagnostic only (wrong results): stages loaded once, then reused
-        if (it >= kStages) {
-          if (leader) ptx::mbar_arrive(&kv_full[s]);
-          return false;
-        }
-#endif
         if (leader) ptx::mbar_arrive_expect_tx(&kv_full[s], 2 * kStageBytes);
         return true;
       };
@@ -315,13 +309,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
 #ifdef CQS_DBG_TIMING
         dc[0] += ts1 - ts0, dc[2] += 1;
 #endif
-#ifdef CQS_DBG_NO_SMX   // diagnostic only (wrong results): no softmax work, only the barrier chain
-        m = 0.f, l = 1.f;
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_leader_a(a_pfull);
-        continue;
-#endif
         uint32_t sr[kBN];
 #pragma unroll
         for (int c = 0; c < kBN / 32; ++c)
@@ -358,21 +345,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair::kThreads, 1)
                                           fmaxf(fmaxf(s[2 * i], s[2 * i + 1]),
                                                 fmaxf(s[2 * i + 2], s[2 * i + 3])));
               float x0, x1;
-#ifdef CQS_DBG_NO_EXP   // diagnostic only (wrong results): P = raw S, no exponentials
-              x0 = s[2 * i], x1 = s[2 * i + 1];
-              if (false) {
-#else
               ptx::f2_split(ptx::ffma2(ptx::f2(s[2 * i], s[2 * i + 1]), sc2, nm2), x0, x1);
               if ((kPolyMask >> (i & 7)) & 1) {
-#endif
                 ptx::exp2_poly_pair(x0, x1);
                 if (2 * i >= valid) x0 = 0.f;   // masked tail columns (poly gives 2^-125)
                 if (2 * i + 1 >= valid) x1 = 0.f;
               } else {
-#ifndef CQS_DBG_NO_EXP
                 x0 = ptx::ex2(x0);
                 x1 = ptx::ex2(x1);
-#endif
               }
               rs2[ii & 3] = ptx::fadd2(rs2[ii & 3], ptx::f2(x0, x1));
               pk[ii] = ptx::pack_bf16(x0, x1);
